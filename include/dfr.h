@@ -1,0 +1,135 @@
+/*
+ * dfr.h — C ABI of the B200-native Diverting Fast Radix (DFR) sort.
+ *
+ * Method: PAPER.md (arXiv 2207.14334, "ThielSort") §3 Alg. 4:
+ * estimate the top passes p (read as SPEC S:284: least p >= 0 with
+ * n <= N_d * 256^p), run an LSD radix sort over those top p digits (
+ * each pass = count -> exclusive prefix -> stable deal, §2),
+ * scan for large buckets, divert runs of small buckets to a simple
+ * stable sort (insertion-sort semantics P:194), recurse on
+ * large buckets with the remaining digits.  Radix M = 256
+ * (P:324), N_d = 64.  Every step is stable, so the result is
+ * THE stable sort of the input by key.
+ *
+ * All entry points:
+ *   - take DEVICE pointers owned by the caller (never freed by the library);
+ *   - sort ascending, in place: on return-and-stream-sync the sorted data is
+ *     in the caller's buffer(s);
+ *   - are asynchronous and stream-ordered on `stream` (0 = legacy default
+ *     stream); they perform no host<->device copy and no host synchronisation
+ *     (except the _ex variants when `stats` is non-NULL, which synchronise
+ *     `stream` to read the counters back);
+ *   - allocate their scratch (a buffer the size of the input, Alg. 4
+ *     l.2, plus counters/queues) with cudaMallocAsync/cudaFreeAsync on
+ *     `stream` inside the call (the paper times allocation);
+ *   - are reentrant: concurrent calls on distinct streams and buffers are safe.
+ *
+ * Errors: 0 (DFR_OK) or a negative code below.  Kernel execution faults
+ * surface at the caller's next synchronisation (CUDA convention).  No C++
+ * exception crosses the ABI.
+ */
+#ifndef DFR_H_
+#define DFR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* dfr_stream_t; /* == cudaStream_t */
+
+enum {
+  DFR_OK = 0,
+  DFR_ERR_INVALID = -1,   /* NULL pointer with n > 0, misaligned element pointer,
+                             overlapping keys/values, or a bad dfr_config field */
+  DFR_ERR_ALLOC = -2,     /* scratch allocation failed (SPEC's "resource error") */
+  DFR_ERR_CUDA = -3,      /* a CUDA launch/configuration error (cudaGetLastError) */
+  DFR_ERR_TOO_LARGE = -4  /* n >= 2^30 (the packed 30-bit look-back counts) */
+};
+
+/* Limits of this build. */
+#define DFR_MAX_N ((size_t)1 << 30) /* exclusive */
+#define DFR_RADIX_BITS 8            /* M = 256 */
+#define DFR_DEFAULT_ND 64           /* diversion threshold N_d */
+
+/* Optional configuration for the _ex entry points (NULL = defaults). */
+typedef struct dfr_config {
+  uint32_t n_d;         /* diversion threshold N_d, 1 <= n_d <= 256 (default 64) */
+  uint32_t skip_trivial_passes; /* 1 (default): skip a pass whose digit histogram has
+                                   one non-empty bin — the identity permutation
+                                   ("skipping unneeded passes"); 0: run every
+                                   pass as Alg. 4 l.6 writes it.  Output identical. */
+} dfr_config;
+
+/* Optional device-side counters, read back (with a stream sync) by _ex. */
+typedef struct dfr_stats {
+  uint32_t level0_p;          /* top passes p at the top call (Alg. 4 l.4) */
+  uint32_t level0_passes_run; /* of those, passes actually executed (not skipped) */
+  uint64_t level0_large;      /* buckets > N_d found by the level-0 scan (l.8-9) */
+  uint64_t mid_buckets;       /* buckets N_d < s <= 4096 finished on-chip (all levels) */
+  uint64_t global_segments;   /* buckets > 4096 recursed through the global queue */
+  uint32_t levels;            /* recursion levels executed after level 0 */
+  uint32_t reserved;
+} dfr_stats;
+
+/*
+ * Sort n uint32 keys at d_keys (4-byte aligned device pointer) in place.
+ * Digits: D = 4 (u32).  Returns DFR_OK for n <= 1 without launching.
+ */
+int dfr_sort_u32(uint32_t* d_keys, size_t n, dfr_stream_t stream);
+
+/* Sort n uint64 keys at d_keys (8-byte aligned device pointer) in place. D = 8. */
+int dfr_sort_u64(uint64_t* d_keys, size_t n, dfr_stream_t stream);
+
+/*
+ * Stable sort of n (uint32 key, uint32 value) pairs held as two arrays
+ * (SoA).  d_vals[i] moves with d_keys[i]; equal keys keep their input order
+ * (stability).  Keys and values must not overlap.
+ */
+int dfr_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_vals, size_t n, dfr_stream_t stream);
+
+/* Same as above with a configuration and optional stats (stats != NULL
+ * synchronises `stream`). */
+int dfr_sort_u32_ex(uint32_t* d_keys, size_t n, dfr_stream_t stream, const dfr_config* cfg,
+                    dfr_stats* stats);
+int dfr_sort_u64_ex(uint64_t* d_keys, size_t n, dfr_stream_t stream, const dfr_config* cfg,
+                    dfr_stats* stats);
+int dfr_sort_pairs_u32_ex(uint32_t* d_keys, uint32_t* d_vals, size_t n, dfr_stream_t stream,
+                          const dfr_config* cfg, dfr_stats* stats);
+
+/*
+ * Stage entry points, exported so each kernel can be checked against the
+ * oracle in isolation.  All take device pointers and run on `stream`.
+ *
+ * dfr_histogram_u32/u64: counts of digits digit_lo .. digit_lo+p-1 (radix 256,
+ *   digit 0 least significant) over n keys into d_counts[p][256]
+ *   (uint32, overwritten).  1 <= p <= 4, digit_lo + p <= D.
+ * dfr_partition_pass_u64 / _pairs_u32: ONE stable counting-sort pass
+ *    on digit d: d_in -> d_out (distinct buffers, n elements);
+ *   d_vals_in/out may be NULL for keys-only u32 use of the pairs variant.
+ */
+int dfr_histogram_u32(const uint32_t* d_keys, size_t n, int digit_lo, int p, uint32_t* d_counts,
+                      dfr_stream_t stream);
+int dfr_histogram_u64(const uint64_t* d_keys, size_t n, int digit_lo, int p, uint32_t* d_counts,
+                      dfr_stream_t stream);
+int dfr_partition_pass_u64(const uint64_t* d_in, uint64_t* d_out, size_t n, int d,
+                           dfr_stream_t stream);
+int dfr_partition_pass_pairs_u32(const uint32_t* d_keys_in, const uint32_t* d_vals_in,
+                                 uint32_t* d_keys_out, uint32_t* d_vals_out, size_t n, int d,
+                                 dfr_stream_t stream);
+
+/* Number of top passes the planner uses for n keys (Alg. 4 l.4), capped at D. */
+int dfr_top_passes(size_t n, int key_bytes, uint32_t n_d);
+
+/* Bytes of scratch one call allocates for n elements of the given widths. */
+size_t dfr_workspace_bytes(size_t n, int key_bytes, int val_bytes);
+
+/* Static string for a status code. */
+const char* dfr_status_string(int status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DFR_H_ */

@@ -1,0 +1,454 @@
+// dfr.cu — kernels, host planner and C ABI of the B200 DFR sort.
+//
+// Launch sequence of one call (all on the caller's stream, no host sync):
+//   cudaMallocAsync(workspace)
+//   k_init     seed the level-0 segment (the whole input) and plan it
+//   k_hist     one read: the p group-digit histograms + diff mask (Alg. 4 l.4-5)
+//   k_plan2    counts -> bucket offsets; identity passes skipped
+//   k_scatter  x p (host knows p for level 0): stable deals, LSD order (l.6)
+//   k_divert   scan for large buckets; small ones sorted on-chip (l.7-14)
+//   k_levels   cooperative kernel: recursion levels 1.. on the global
+//              segment queue (l.11), looping on the device while it is non-empty
+//   k_mid      buckets N_d < s <= C finished in shared memory
+//   cudaFreeAsync(workspace)
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "dfr.h"
+#include "dfr_phases.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dfr {
+
+// ------------------------------------------------------------------ kernels
+template <class K, bool PAIRS>
+__global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params<K> P, uint32_t n) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  Ctl* c = P.ctl;
+  if (threadIdx.x == 0) {
+    memset(c, 0, sizeof(Ctl));
+    c->level = ~0u;
+    c->cur = 0;
+    c->next_count = 1;
+    Seg s = {};
+    s.start = 0;
+    s.len = n;
+    s.hi = P.D - 1;
+    s.buf = 0;
+    P.segq[1][0] = s;
+  }
+  __syncthreads();
+  Phases<K, PAIRS>::plan(P, sm);
+}
+
+// stage API: a single segment with a forced group (digit_lo .. digit_lo+p-1)
+template <class K, bool PAIRS>
+__global__ void __launch_bounds__(THREADS) k_init_stage(Params<K> P, uint32_t n, int digit_lo,
+                                                        int p) {
+  Ctl* c = P.ctl;
+  if (threadIdx.x == 0) {
+    memset(c, 0, sizeof(Ctl));
+    c->cur = 0;
+    c->nseg = 1;
+    c->total_tiles = (n + TILE - 1) / TILE;
+    c->total_chunks = 0;
+    c->max_p = p;
+    Seg s = {};
+    s.start = 0;
+    s.len = n;
+    s.hi = digit_lo + p - 1;
+    s.p = p;
+    s.low = digit_lo;
+    s.ntiles = c->total_tiles;
+    s.final_buf = 0;
+    P.segq[0][0] = s;
+  }
+  for (int r = 0; r < p; ++r) P.hist[r * 256 + threadIdx.x] = 0;
+}
+
+template <class K, bool PAIRS>
+__global__ void __launch_bounds__(THREADS) k_hist(const __grid_constant__ Params<K> P) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  Phases<K, PAIRS>::hist(P, sm);
+}
+
+template <class K, bool PAIRS>
+__global__ void __launch_bounds__(THREADS) k_plan2(const __grid_constant__ Params<K> P) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  Phases<K, PAIRS>::plan2(P, sm);
+}
+
+template <class K, bool PAIRS>
+__global__ void __launch_bounds__(THREADS) k_scatter(const __grid_constant__ Params<K> P, int j) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  Phases<K, PAIRS>::scatter(P, j, sm);
+}
+
+template <class K, bool PAIRS>
+__global__ void __launch_bounds__(THREADS) k_divert(const __grid_constant__ Params<K> P) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  Phases<K, PAIRS>::divert(P, sm);
+}
+
+template <class K, bool PAIRS>
+__global__ void __launch_bounds__(THREADS) k_mid(const __grid_constant__ Params<K> P) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  Phases<K, PAIRS>::mid(P, sm);
+}
+
+// Recursion levels 1.. (Alg. 4 l.11 applied to every queued large bucket at
+// once).  Cooperative launch: every CTA is resident, levels are separated by
+// grid-wide barriers, and the loop ends on the device when the queue is empty.
+template <class K, bool PAIRS>
+__global__ void __launch_bounds__(THREADS) k_levels(const __grid_constant__ Params<K> P) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  cg::grid_group grid = cg::this_grid();
+  using Ph = Phases<K, PAIRS>;
+  for (int level = 1; level < 2 * P.D; ++level) {
+    if (*(volatile uint32_t*)&P.ctl->next_count == 0) break;
+    grid.sync();
+    if (blockIdx.x == 0) Ph::plan(P, sm);
+    grid.sync();
+    Ph::hist(P, sm);
+    grid.sync();
+    Ph::plan2(P, sm);
+    grid.sync();
+    for (int j = 0; j < MAX_PASSES; ++j) {
+      if ((uint32_t)j >= *(volatile uint32_t*)&P.ctl->max_p) break;
+      Ph::scatter(P, j, sm);
+      grid.sync();
+    }
+    Ph::divert(P, sm);
+    grid.sync();
+  }
+}
+
+template <class K, bool PAIRS>
+__global__ void k_seed_mid(Params<K> P, uint32_t n) {
+  Ctl* c = P.ctl;
+  memset(c, 0, sizeof(Ctl));
+  MidE m;
+  m.start = 0;
+  m.len = (uint16_t)n;
+  m.hi = (int8_t)(P.D - 1);
+  m.buf = 0;
+  P.midq[0] = m;
+  c->mid_count = 1;
+}
+
+// ------------------------------------------------------------------ host
+struct Dev {
+  int sms = 0;
+  int occ_hist = 0, occ_scatter = 0, occ_divert = 0, occ_mid = 0, occ_levels = 0;
+};
+
+template <class K, bool PAIRS>
+static cudaError_t get_dev(Dev& out) {
+  using Ph = Phases<K, PAIRS>;
+  static std::once_flag once[16];
+  static Dev devs[16];
+  static cudaError_t errs[16];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+  std::call_once(once[dev], [&]() {
+    Dev d;
+    cudaError_t err = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    auto setup = [&](const void* f, size_t smem, int* occ) {
+      if (err != cudaSuccess) return;
+      err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, f, THREADS, smem);
+    };
+    setup((const void*)k_init<K, PAIRS>, 64, &d.occ_hist);
+    setup((const void*)k_hist<K, PAIRS>, Ph::SMEM_HIST, &d.occ_hist);
+    setup((const void*)k_plan2<K, PAIRS>, 64, &d.occ_mid);
+    setup((const void*)k_scatter<K, PAIRS>, Ph::SMEM_SCATTER, &d.occ_scatter);
+    setup((const void*)k_divert<K, PAIRS>, Ph::SMEM_DIVERT, &d.occ_divert);
+    setup((const void*)k_mid<K, PAIRS>, Ph::SMEM_MID, &d.occ_mid);
+    setup((const void*)k_levels<K, PAIRS>, Ph::SMEM_LEVEL, &d.occ_levels);
+    devs[dev] = d;
+    errs[dev] = err;
+  });
+  out = devs[dev];
+  return errs[dev];
+}
+
+static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  size_t b_keys, b_vals, ctl, segq0, segq1, midq, hist, status, total;
+  size_t max_segs, mid_cap, hist_rows, tiles_max;
+};
+
+static Layout make_layout(size_t n, int kb, int vb, uint32_t n_d, int min_passes = 1) {
+  Layout L{};
+  L.max_segs = n / (MID_CAP + 1) + 2;
+  L.mid_cap = n / (n_d + 1) + 2;
+  // rows: sum of p over the segments of one level (p = 1 + [len > n_d*2^8] + ...)
+  L.hist_rows = MAX_PASSES + L.max_segs;
+  for (uint64_t cap = (uint64_t)n_d << 8; cap < n; cap <<= 8) L.hist_rows += n / (cap + 1) + 1;
+  L.tiles_max = 2 * (n / TILE) + L.max_segs + 2;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes);
+    return o;
+  };
+  L.b_keys = take(n * kb);
+  L.b_vals = vb ? take(n * vb) : 0;
+  L.ctl = take(sizeof(Ctl));
+  L.segq0 = take(L.max_segs * sizeof(Seg));
+  L.segq1 = take(L.max_segs * sizeof(Seg));
+  L.midq = take(L.mid_cap * sizeof(MidE));
+  L.hist = take(L.hist_rows * 256 * 4);
+  int passes = est_top_passes(n, n_d);  // no group of any level has more passes
+  passes = passes < min_passes ? min_passes : (passes > MAX_PASSES ? MAX_PASSES : passes);
+  L.status = take((size_t)passes * L.tiles_max * 256 * 4);
+  L.total = off;
+  return L;
+}
+
+template <class K>
+static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals, bool pairs,
+                             uint32_t n_d, uint32_t skip) {
+  Params<K> P{};
+  P.A = keys;
+  P.B = reinterpret_cast<K*>(ws + L.b_keys);
+  P.Av = vals;
+  P.Bv = pairs ? reinterpret_cast<uint32_t*>(ws + L.b_vals) : nullptr;
+  P.ctl = reinterpret_cast<Ctl*>(ws + L.ctl);
+  P.segq[0] = reinterpret_cast<Seg*>(ws + L.segq0);
+  P.segq[1] = reinterpret_cast<Seg*>(ws + L.segq1);
+  P.midq = reinterpret_cast<MidE*>(ws + L.midq);
+  P.hist = reinterpret_cast<uint32_t*>(ws + L.hist);
+  P.status = reinterpret_cast<uint32_t*>(ws + L.status);
+  P.status_stride = L.tiles_max * 256;
+  P.max_segs = (uint32_t)L.max_segs;
+  P.mid_cap = (uint32_t)L.mid_cap;
+  P.hist_rows = (uint32_t)L.hist_rows;
+  P.n_d = n_d;
+  P.chunk = WIN - 1 - n_d;
+  P.skip_trivial = skip;
+  P.D = (int)sizeof(K);
+  return P;
+}
+
+static int cfg_nd(const dfr_config* cfg, uint32_t* n_d, uint32_t* skip) {
+  *n_d = DFR_DEFAULT_ND;
+  *skip = 1;
+  if (cfg) {
+    *n_d = cfg->n_d ? cfg->n_d : DFR_DEFAULT_ND;
+    *skip = cfg->skip_trivial_passes ? 1 : 0;
+  }
+  if (*n_d < 8 || *n_d > (uint32_t)MAX_ND) return DFR_ERR_INVALID;
+  return DFR_OK;
+}
+
+template <class K, bool PAIRS>
+static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const dfr_config* cfg,
+                     dfr_stats* stats) {
+  using Ph = Phases<K, PAIRS>;
+  uint32_t n_d, skip;
+  if (cfg_nd(cfg, &n_d, &skip) != DFR_OK) return DFR_ERR_INVALID;
+  if (stats) memset(stats, 0, sizeof(*stats));
+  if (n <= 1) return DFR_OK;
+  if (!keys || (PAIRS && !vals)) return DFR_ERR_INVALID;
+  if (reinterpret_cast<uintptr_t>(keys) % sizeof(K)) return DFR_ERR_INVALID;
+  if (PAIRS) {
+    if (reinterpret_cast<uintptr_t>(vals) % 4) return DFR_ERR_INVALID;
+    const char* ka = reinterpret_cast<const char*>(keys);
+    const char* va = reinterpret_cast<const char*>(vals);
+    if (ka < va + n * 4 && va < ka + n * sizeof(K)) return DFR_ERR_INVALID;
+  }
+  if (n >= DFR_MAX_N) return DFR_ERR_TOO_LARGE;
+  Dev dv;
+  if (get_dev<K, PAIRS>(dv) != cudaSuccess) return DFR_ERR_CUDA;
+  cudaGetLastError();
+
+  const Layout L = make_layout(n, sizeof(K), PAIRS ? 4 : 0, n_d);
+  char* ws = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&ws), L.total, st) != cudaSuccess) {
+    cudaGetLastError();
+    return DFR_ERR_ALLOC;
+  }
+  Params<K> P = make_params<K>(ws, L, keys, vals, PAIRS, n_d, skip);
+  const uint32_t nn = (uint32_t)n;
+  const int sms = dv.sms;
+
+  if (n <= (size_t)MID_CAP) {  // the whole input fits one on-chip DFR
+    k_seed_mid<K, PAIRS><<<1, 1, 0, st>>>(P, nn);
+    k_mid<K, PAIRS><<<1, THREADS, Ph::SMEM_MID, st>>>(P);
+  } else {
+    int p0 = est_top_passes(n, n_d);
+    if (p0 > (int)sizeof(K)) p0 = (int)sizeof(K);
+    const uint32_t tiles = (nn + TILE - 1) / TILE;
+    k_init<K, PAIRS><<<1, THREADS, 64, st>>>(P, nn);
+    const int g_hist = (int)std::min<uint32_t>(tiles, (uint32_t)(sms * std::max(1, dv.occ_hist)));
+    k_hist<K, PAIRS><<<g_hist, THREADS, Ph::SMEM_HIST, st>>>(P);
+    k_plan2<K, PAIRS><<<1, THREADS, 64, st>>>(P);
+    const int g_sc = (int)std::min<uint32_t>(tiles, (uint32_t)(sms * std::max(1, dv.occ_scatter)));
+    for (int j = 0; j < p0; ++j) k_scatter<K, PAIRS><<<g_sc, THREADS, Ph::SMEM_SCATTER, st>>>(P, j);
+    const uint32_t chunks = (nn + P.chunk - 1) / P.chunk;
+    const int g_dv = (int)std::min<uint32_t>(chunks, (uint32_t)(sms * std::max(1, dv.occ_divert)));
+    k_divert<K, PAIRS><<<g_dv, THREADS, Ph::SMEM_DIVERT, st>>>(P);
+    if (n > (size_t)MID_CAP) {
+      void* args[] = {&P};
+      const int g_lv = sms * std::max(1, dv.occ_levels);
+      cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_levels<K, PAIRS>, g_lv, THREADS,
+                                                  args, Ph::SMEM_LEVEL, st);
+      if (e != cudaSuccess) {
+        cudaFreeAsync(ws, st);
+        return DFR_ERR_CUDA;
+      }
+    }
+    const int g_mid = sms * std::max(1, dv.occ_mid);
+    k_mid<K, PAIRS><<<g_mid, THREADS, Ph::SMEM_MID, st>>>(P);
+  }
+  cudaError_t e = cudaGetLastError();
+  int rc = (e == cudaSuccess) ? DFR_OK : DFR_ERR_CUDA;
+  if (stats && rc == DFR_OK) {
+    Ctl h;
+    if (cudaMemcpyAsync(&h, P.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      rc = DFR_ERR_CUDA;
+    } else {
+      stats->level0_p = h.level0_p;
+      stats->level0_passes_run = h.level0_run;
+      stats->level0_large = h.level0_large;
+      stats->mid_buckets = h.mid_buckets;
+      stats->global_segments = h.global_segments;
+      stats->levels = h.levels_run;
+      stats->reserved = h.overflow;
+    }
+  }
+  if (cudaFreeAsync(ws, st) != cudaSuccess && rc == DFR_OK) rc = DFR_ERR_CUDA;
+  return rc;
+}
+
+// stage API helpers
+template <class K, bool PAIRS>
+static int stage_impl(const K* in, const uint32_t* vin, K* out, uint32_t* vout, size_t n,
+                      int digit_lo, int p, uint32_t* d_counts, cudaStream_t st) {
+  using Ph = Phases<K, PAIRS>;
+  if (n == 0) return DFR_OK;
+  if (n >= DFR_MAX_N) return DFR_ERR_TOO_LARGE;
+  if (!in || p < 1 || p > MAX_PASSES || digit_lo < 0 || digit_lo + p > (int)sizeof(K))
+    return DFR_ERR_INVALID;
+  Dev dv;
+  if (get_dev<K, PAIRS>(dv) != cudaSuccess) return DFR_ERR_CUDA;
+  cudaGetLastError();
+  const Layout L = make_layout(n, 0, 0, 64, MAX_PASSES);
+  char* ws = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&ws), L.total, st) != cudaSuccess) {
+    cudaGetLastError();
+    return DFR_ERR_ALLOC;
+  }
+  Params<K> P = make_params<K>(ws, L, const_cast<K*>(in), const_cast<uint32_t*>(vin), PAIRS, 64, 0);
+  P.B = out;  // pass 0 deals A=in -> B=out
+  P.Bv = vout;
+  const uint32_t nn = (uint32_t)n;
+  const uint32_t tiles = (nn + TILE - 1) / TILE;
+  k_init_stage<K, PAIRS><<<1, THREADS, 0, st>>>(P, nn, digit_lo, p);
+  const int g_hist = (int)std::min<uint32_t>(tiles, (uint32_t)(dv.sms * std::max(1, dv.occ_hist)));
+  k_hist<K, PAIRS><<<g_hist, THREADS, Ph::SMEM_HIST, st>>>(P);
+  if (d_counts) {
+    cudaMemcpyAsync(d_counts, P.hist, (size_t)p * 256 * 4, cudaMemcpyDeviceToDevice, st);
+  } else {
+    k_plan2<K, PAIRS><<<1, THREADS, 64, st>>>(P);
+    const int g_sc = (int)std::min<uint32_t>(tiles, (uint32_t)(dv.sms * std::max(1, dv.occ_scatter)));
+    k_scatter<K, PAIRS><<<g_sc, THREADS, Ph::SMEM_SCATTER, st>>>(P, 0);
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(ws, st);
+  return e == cudaSuccess ? DFR_OK : DFR_ERR_CUDA;
+}
+
+}  // namespace dfr
+
+// -------------------------------------------------------------------- C ABI
+extern "C" {
+
+int dfr_sort_u32_ex(uint32_t* d_keys, size_t n, dfr_stream_t stream, const dfr_config* cfg,
+                    dfr_stats* stats) {
+  return dfr::sort_impl<uint32_t, false>(d_keys, nullptr, n, (cudaStream_t)stream, cfg, stats);
+}
+int dfr_sort_u64_ex(uint64_t* d_keys, size_t n, dfr_stream_t stream, const dfr_config* cfg,
+                    dfr_stats* stats) {
+  return dfr::sort_impl<unsigned long long, false>(reinterpret_cast<unsigned long long*>(d_keys),
+                                                   nullptr, n, (cudaStream_t)stream, cfg, stats);
+}
+int dfr_sort_pairs_u32_ex(uint32_t* d_keys, uint32_t* d_vals, size_t n, dfr_stream_t stream,
+                          const dfr_config* cfg, dfr_stats* stats) {
+  return dfr::sort_impl<uint32_t, true>(d_keys, d_vals, n, (cudaStream_t)stream, cfg, stats);
+}
+int dfr_sort_u32(uint32_t* d_keys, size_t n, dfr_stream_t stream) {
+  return dfr_sort_u32_ex(d_keys, n, stream, nullptr, nullptr);
+}
+int dfr_sort_u64(uint64_t* d_keys, size_t n, dfr_stream_t stream) {
+  return dfr_sort_u64_ex(d_keys, n, stream, nullptr, nullptr);
+}
+int dfr_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_vals, size_t n, dfr_stream_t stream) {
+  return dfr_sort_pairs_u32_ex(d_keys, d_vals, n, stream, nullptr, nullptr);
+}
+
+int dfr_histogram_u32(const uint32_t* d_keys, size_t n, int digit_lo, int p, uint32_t* d_counts,
+                      dfr_stream_t stream) {
+  if (!d_counts) return DFR_ERR_INVALID;
+  return dfr::stage_impl<uint32_t, false>(d_keys, nullptr, nullptr, nullptr, n, digit_lo, p,
+                                          d_counts, (cudaStream_t)stream);
+}
+int dfr_histogram_u64(const uint64_t* d_keys, size_t n, int digit_lo, int p, uint32_t* d_counts,
+                      dfr_stream_t stream) {
+  if (!d_counts) return DFR_ERR_INVALID;
+  return dfr::stage_impl<unsigned long long, false>(
+      reinterpret_cast<const unsigned long long*>(d_keys), nullptr, nullptr, nullptr, n, digit_lo,
+      p, d_counts, (cudaStream_t)stream);
+}
+int dfr_partition_pass_u64(const uint64_t* d_in, uint64_t* d_out, size_t n, int d,
+                           dfr_stream_t stream) {
+  if (n && (!d_in || !d_out || d_in == d_out)) return DFR_ERR_INVALID;
+  return dfr::stage_impl<unsigned long long, false>(
+      reinterpret_cast<const unsigned long long*>(d_in), nullptr,
+      reinterpret_cast<unsigned long long*>(d_out), nullptr, n, d, 1, nullptr,
+      (cudaStream_t)stream);
+}
+int dfr_partition_pass_pairs_u32(const uint32_t* d_keys_in, const uint32_t* d_vals_in,
+                                 uint32_t* d_keys_out, uint32_t* d_vals_out, size_t n, int d,
+                                 dfr_stream_t stream) {
+  if (n && (!d_keys_in || !d_keys_out || d_keys_in == d_keys_out)) return DFR_ERR_INVALID;
+  if ((d_vals_in == nullptr) != (d_vals_out == nullptr)) return DFR_ERR_INVALID;
+  if (d_vals_in)
+    return dfr::stage_impl<uint32_t, true>(d_keys_in, d_vals_in, d_keys_out, d_vals_out, n, d, 1,
+                                           nullptr, (cudaStream_t)stream);
+  return dfr::stage_impl<uint32_t, false>(d_keys_in, nullptr, d_keys_out, nullptr, n, d, 1,
+                                          nullptr, (cudaStream_t)stream);
+}
+
+int dfr_top_passes(size_t n, int key_bytes, uint32_t n_d) {
+  if (n_d == 0) n_d = DFR_DEFAULT_ND;
+  int p = dfr::est_top_passes(n, n_d);
+  return p > key_bytes ? key_bytes : p;
+}
+
+size_t dfr_workspace_bytes(size_t n, int key_bytes, int val_bytes) {
+  return dfr::make_layout(n, key_bytes, val_bytes, DFR_DEFAULT_ND).total;
+}
+
+const char* dfr_status_string(int status) {
+  switch (status) {
+    case DFR_OK: return "DFR_OK";
+    case DFR_ERR_INVALID: return "DFR_ERR_INVALID";
+    case DFR_ERR_ALLOC: return "DFR_ERR_ALLOC";
+    case DFR_ERR_CUDA: return "DFR_ERR_CUDA";
+    case DFR_ERR_TOO_LARGE: return "DFR_ERR_TOO_LARGE";
+    default: return "DFR_ERR_UNKNOWN";
+  }
+}
+
+}  // extern "C"

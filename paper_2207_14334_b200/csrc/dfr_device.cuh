@@ -1,0 +1,244 @@
+// dfr_device.cuh — device building blocks of the B200 DFR sort (sm_100a).
+//
+// Citations: P:L = PAPER.md line L (arXiv 2207.14334), S:L = SPEC.md line L.
+// Shares nothing with oracle/ (test infrastructure).
+//
+// Vocabulary (§2): a *pass* processes every record of a
+// range on one digit; a *count* builds per-digit histograms; the *deal*
+// places records into *buckets*.  A *segment* here is one DFR invocation
+// (Alg. 4) on a contiguous bucket: the whole input at level 0,
+// a large bucket (Alg. 4 l.11 "recurse on the large bucket") at level >= 1.
+#pragma once
+#include <cooperative_groups.h>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dfr {
+
+constexpr int THREADS = 256;             // one CTA = 8 warps
+constexpr int WARPS = THREADS / 32;
+constexpr int KPT = 16;                  // keys per thread per tile
+constexpr int TILE = THREADS * KPT;      // 4096 keys per tile (hist / deal)
+constexpr int WIN = TILE;                // diversion window (keys) per CTA
+constexpr int MID_CAP = 4096;            // C: buckets N_d < s <= C finish on-chip
+constexpr int MAX_ND = 256;              // composite index uses 8 bits
+constexpr int MAX_PASSES = 4;            // top passes per group (p <= 3 for n < 2^30)
+constexpr uint32_t FLAG_AGG = 1u << 30;  // look-back: tile aggregate available
+constexpr uint32_t FLAG_INC = 2u << 30;  // look-back: inclusive prefix available
+constexpr uint32_t VAL_MASK = (1u << 30) - 1;
+
+// Seg::flags
+constexpr uint32_t SEG_SKIP_DIVERT = 1u << 8;  // no diversion scan this level
+constexpr uint32_t SEG_COPY = 1u << 9;         // finished, data in B: copy to A
+constexpr uint32_t SEG_DONE = 1u << 10;        // finished in A
+
+struct Seg {                    // one DFR invocation on a contiguous bucket
+  uint32_t start, len;          // element range in the arrays
+  int32_t hi;                   // top remaining digit; digits above are constant
+  uint32_t buf;                 // 0: data in A (caller), 1: data in B (scratch)
+  uint32_t p;                   // top passes of this invocation (Alg. 4 l.4)
+  int32_t low;                  // lowest digit of the group = hi - p + 1
+  uint32_t tile0;               // first tile id (exclusive prefix over segments)
+  uint32_t chunk0;              // first diversion chunk id
+  uint32_t hist_off;            // first histogram row (one row of 256 per pass)
+  uint32_t flags;               // bits 0..3: pass j skipped; SEG_* above
+  uint32_t final_buf;           // buffer holding the data after the passes
+  uint32_t ntiles;              // tiles of this segment
+  unsigned long long diff;      // OR over the segment of (key ^ key[start])
+  uint32_t pad[2];
+};
+static_assert(sizeof(Seg) == 64, "Seg layout");
+
+struct MidE {                   // a bucket N_d < len <= C finished on-chip
+  uint32_t start;
+  uint16_t len;
+  int8_t hi;
+  uint8_t buf;
+};
+
+struct Ctl {
+  uint32_t cur;                 // index of the current segment queue (0/1)
+  uint32_t nseg;                // segments in the current level
+  uint32_t total_tiles;
+  uint32_t total_chunks;
+  uint32_t ticket[MAX_PASSES];  // dynamic tile tickets per pass (forward progress)
+  uint32_t next_count;          // segments queued for the next level
+  uint32_t mid_count;           // mid buckets queued (all levels)
+  uint32_t level;               // current level (0 = top call)
+  uint32_t overflow;            // queue overflow guard (should stay 0)
+  unsigned long long level0_large;
+  unsigned long long mid_buckets;
+  unsigned long long global_segments;
+  uint32_t level0_p, level0_run;
+  uint32_t levels_run, max_p;
+};
+
+template <class K>
+struct Params {
+  K* A;                 // caller keys
+  K* B;                 // scratch keys ("buffer the same size as the input")
+  uint32_t* Av;         // caller values (pairs) or null
+  uint32_t* Bv;         // scratch values or null
+  Ctl* ctl;
+  Seg* segq[2];
+  MidE* midq;
+  uint32_t* hist;       // histogram / bucket-offset rows, 256 u32 each
+  uint32_t* status;     // look-back status words [MAX_PASSES][tiles_max][256]
+  size_t status_stride; // words per pass
+  uint32_t max_segs;
+  uint32_t mid_cap;     // capacity of midq
+  uint32_t hist_rows;   // capacity of hist (rows)
+  uint32_t n_d;         // diversion threshold N_d
+  uint32_t chunk;       // diversion chunk = WIN - 1 - n_d
+  uint32_t skip_trivial;
+  int D;                // digits per key
+};
+
+// ------------------------------------------------------------------ helpers
+template <class K>
+__device__ __forceinline__ uint32_t digit_of(K k, int d) {
+  return (uint32_t)(k >> (8 * d)) & 255u;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// least p >= 0 with len <= n_d * 256^p  (Alg. 4 l.4; reading S:284)
+__host__ __device__ __forceinline__ int est_top_passes(uint64_t len, uint32_t n_d) {
+  int p = 0;
+  uint64_t cap = n_d;
+  while (len > cap && p < 8) {
+    cap = (cap > (~0ull >> 8)) ? ~0ull : (cap << 8);
+    ++p;
+  }
+  return p;
+}
+
+// highest digit index <= hi whose byte of `diff` is non-zero, or -1
+__device__ __forceinline__ int highest_nonconst(unsigned long long diff, int hi) {
+  for (int d = hi; d >= 0; --d)
+    if ((diff >> (8 * d)) & 255ull) return d;
+  return -1;
+}
+
+// exclusive block scan of one value per thread (THREADS threads); returns the
+// exclusive prefix, writes the block total to *total (all threads).
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp,
+                                                    uint32_t* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = lane < WARPS ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < WARPS; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < WARPS) s_warp[lane] = t;  // inclusive per warp
+  }
+  __syncthreads();
+  uint32_t wpre = w ? s_warp[w - 1] : 0;
+  *total = s_warp[WARPS - 1];
+  __syncthreads();
+  return wpre + x - v;
+}
+
+// Warp-level multi-split rank (stable): items are (j, lane) in j-major order;
+// rank[j] = number of earlier items of this warp with the same digit.
+// whist (256 u32 for this warp, zeroed) accumulates the warp's digit counts.
+// Digits >= 256 mark invalid items (not counted).
+template <int N>
+__device__ __forceinline__ void warp_rank(const uint32_t (&dig)[N], uint32_t (&rank)[N],
+                                          uint32_t* whist) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const uint32_t d = dig[j];
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (lane == leader && d < 256) {
+      base = whist[d];
+      whist[d] = base + __popc(peers);
+    }
+    base = __shfl_sync(0xffffffffu, base, leader);
+    rank[j] = base + __popc(peers & lt);
+    __syncwarp();
+  }
+}
+
+// binary search: largest i in [0, n) with key(i) <= t (key non-decreasing, key(0) = 0)
+template <class F>
+__device__ __forceinline__ uint32_t upper_index(uint32_t n, uint32_t t, F key) {
+  uint32_t lo = 0, hi = n;  // answer in [lo, hi)
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (key(mid) <= t)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// ---- bucket-start bitmask search (diversion) -------------------------------
+// last set bit at position <= i and >= lim, or -1
+__device__ __forceinline__ int prev_set(const uint32_t* bm, int i, int lim) {
+  int w = i >> 5;
+  uint32_t m = bm[w] & (0xffffffffu >> (31 - (i & 31)));
+  while (true) {
+    if (m) {
+      int s = w * 32 + 31 - __clz(m);
+      return s >= lim ? s : -1;
+    }
+    if (--w < 0 || w * 32 + 31 < lim) return -1;
+    m = bm[w];
+  }
+}
+// first set bit at position > i and <= lim (lim < nbits), or -1
+__device__ __forceinline__ int next_set(const uint32_t* bm, int i, int lim) {
+  int p = i + 1;
+  if (p > lim) return -1;
+  int w = p >> 5;
+  uint32_t m = bm[w] & (0xffffffffu << (p & 31));
+  while (true) {
+    if (m) {
+      int e = w * 32 + __ffs(m) - 1;
+      return e <= lim ? e : -1;
+    }
+    ++w;
+    if (w * 32 > lim) return -1;
+    m = bm[w];
+  }
+}
+
+template <class K>
+struct Comp {  // composite (remaining bits, index-in-bucket) for the small sort
+  using T = unsigned long long;
+};
+template <>
+struct Comp<uint32_t> {
+  using T = uint32_t;
+};
+
+}  // namespace dfr
