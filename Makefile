@@ -28,3 +28,7 @@ clean:
 	rm -f $(DFR_SO) $(ORACLE_SO) $(DATAGEN_SO)
 
 .PHONY: all host clean
+
+# debug variant: sync + error check after every launch, device bounds asserts
+paper_2207_14334_b200/libdfr_debug.so: $(DFR_SRC) $(DFR_HDR)
+	$(NVCC) $(NVFLAGS) -DDFR_DEBUG -shared $(DFR_SRC) -o $@

@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200 DFR sort (BASELINE.json metric:
+"Gkeys/s sorting 2^28 uint64 keys on 1 B200; % of HBM roofline").
+
+One step = one complete DFR sort (every hot-path row of SURVEY §8(a): plan,
+histogram, p stable deals, diversion scan + small-bucket sort, recursion,
+on-chip mid buckets) of 2^28 i.i.d. uniform uint64 keys (config c5-uniform,
+SplitMix64 seed 5) already resident in HBM.  Each timed step sorts its own
+pristine resident copy (2 GiB > 126 MB L2, so no step sees a warm L2).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dfr|reference]
+
+N > 1 (torchrun): independent replicas, one per GPU (the path does
+not shard; no data-path collective), timed on the device, max over ranks.
+--impl reference: the CPU oracle (oracle/, the only other place bench.py runs
+it) on a bounded sample of the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gkeys/s sorting 2^28 uint64 keys on 1 B200; % of HBM roofline"
+UNIT = "Gkeys/s"
+# algorithmic bytes per key: one histogram
+# read (8) + p=3 stable deals x (read 8 + write 8) + diversion read+write (16)
+SORT_BYTES_PER_KEY_U64 = 72
+PASS_BYTES_PER_KEY_U64 = 16  # one stable deal of a u64 key: read 8 + write 8
+NOMINAL_HBM_GBS = 8000.0
+FALLBACK_HBM_GBS = 6650.0
+
+THROTTLE_BITS = {0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+                 0x80: "hw_power_brake_slowdown", 0x4: "sw_power_cap", 0x2: "applications_clocks",
+                 0x1: "gpu_idle", 0x10: "sync_boost", 0x100: "display_clock"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="dfr", choices=["dfr", "reference"])
+    ap.add_argument("--case", default="c5-uniform", help="datagen case (default: the headline)")
+    ap.add_argument("--n", type=int, default=None, help="override the case size")
+    ap.add_argument("--quick", action="store_true", help="skip e2e and cpu_baseline (for ncu runs)")
+    ap.add_argument("--out", default=None, help="also append the JSON line to this file")
+    return ap.parse_args()
+
+
+def peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Polls NVML every ~2 ms on a thread while the timed region runs."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(get_r(self.h))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        reasons = [name for bit, name in THROTTLE_BITS.items() if self.reasons & bit]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+def workload(case, n):
+    import datagen
+    c = datagen.CASES[case]
+    n = c.n if n is None else n
+    desc = {
+        "c5-uniform": "2^28 uint64 keys i.i.d. uniform over [0, 2^64) (SplitMix64 seed 5)",
+    }.get(case, f"{case} recipe (datagen.make_case)")
+    if n != c.n:
+        desc += f", n={n}"
+    return c, n, desc
+
+
+def config_dict(case, n, c, desc, n_d=64):
+    return {"workload": f"{case}: {desc}", "n": n, "key": c.key_dtype,
+            "pairs": c.pairs, "n_d": n_d, "radix_bits": 8,
+            "l2": "inputs larger than L2 (2 GiB/step vs 126 MB); each step sorts its own "
+                  "pristine resident copy",
+            "parallelism": "replicas (one independent sort per GPU)"}
+
+
+# ---------------------------------------------------------------- reference
+def run_reference(args, rank, world):
+    """The CPU oracle (plain single-threaded DFR) on a bounded sample per step."""
+    if rank != 0:
+        return
+    import datagen
+    import oracle
+    c, n, desc = workload(args.case, args.n)
+    sample = min(n, 1 << 24)
+    keys, vals = datagen.make_case(args.case, n)
+    keys = keys[:sample].copy()
+    vals = vals[:sample].copy() if vals is not None else None
+    for _ in range(args.warmup):
+        oracle.dfr_sort(keys, vals)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.dfr_sort(keys, vals)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = sample * args.steps / total / 1e9
+    samp = f"first {sample} keys of the {args.case} recipe per step, oracle.dfr_sort (1 thread)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": c.key_dtype, "data": "synthetic",
+            "config": config_dict(args.case, n, c, desc),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": samp},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    emit(line, args)
+
+
+def emit(line, args):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if args.out:
+        with open(args.out, "a") as f:
+            f.write(s + "\n")
+
+
+# ---------------------------------------------------------------- our arm
+def run_dfr(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import datagen
+    import paper_2207_14334_b200 as dfr
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    c, n, desc = workload(args.case, args.n)
+    keys_h, vals_h = datagen.make_case(args.case, n)
+    kdt = np.uint64 if c.key_dtype == "u64" else np.uint32
+    tdt = torch.int64 if c.key_dtype == "u64" else torch.int32
+    kb = np.dtype(kdt).itemsize
+    vb = 4 if c.pairs else 0
+    fp_in = datagen.fingerprint(keys_h)
+
+    pristine = torch.from_numpy(keys_h.view(np.int64 if kb == 8 else np.int32)).to(dev)
+    pristine_v = torch.from_numpy(vals_h.view(np.int32)).to(dev) if c.pairs else None
+    K, W = args.steps, args.warmup
+    free = torch.cuda.mem_get_info(dev)[0]
+    per = n * (kb + vb)
+    nbuf = int(min(K + W, max(2, (free - 3 * per - (4 << 30)) // per)))
+    bufs = [pristine.clone() for _ in range(nbuf)]
+    vbufs = [pristine_v.clone() for _ in range(nbuf)] if c.pairs else [None] * nbuf
+    restore = nbuf < K + W  # not enough HBM for a copy per step: restore between steps
+    stream = torch.cuda.current_stream()
+    nph = len(dfr.PHASES)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nph)] for _ in range(K)]
+    for row in evs:  # torch creates the CUDA event lazily, on its first record
+        for e in row:
+            e.record(stream)
+
+    def sort_step(i, ev=None):
+        b = bufs[i % nbuf]
+        vbuf = vbufs[i % nbuf]
+        dfr.sort(b, vbuf, events=ev)
+
+    for i in range(W):
+        if restore:
+            bufs[i % nbuf].copy_(pristine)
+            if c.pairs:
+                vbufs[i % nbuf].copy_(pristine_v)
+        sort_step(i)
+    torch.cuda.synchronize()
+
+    # ---- timed region: exactly K steps
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ms = []
+    l0 = dfr.launch_counter()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        if not restore:
+            start.record(stream)
+            for i in range(K):
+                sort_step(W + i, evs[i])
+            stop.record(stream)
+            torch.cuda.synchronize()
+            elapsed = start.elapsed_time(stop)
+        else:  # per-step events; the restore copy is outside each step's events
+            for i in range(K):
+                bufs[(W + i) % nbuf].copy_(pristine)
+                if c.pairs:
+                    vbufs[(W + i) % nbuf].copy_(pristine_v)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                sort_step(W + i, evs[i])
+                b.record(stream)
+                torch.cuda.synchronize()
+                step_ms.append(a.elapsed_time(b))
+            elapsed = sum(step_ms)
+    launches = dfr.launch_counter() - l0
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+
+    # per-phase device times (CUDA events recorded by the library on this stream)
+    phase_ms = {}
+    for p, name in enumerate(dfr.PHASES):
+        phase_ms[name] = statistics.mean(evs[i][2 * p].elapsed_time(evs[i][2 * p + 1]) for i in range(K))
+
+    # verification of the last output: non-decreasing + same multiset as the input
+    last = bufs[(W + K - 1) % nbuf]
+    out_h = last.cpu().numpy().view(kdt)
+    verified = bool(datagen.is_sorted(out_h) and datagen.fingerprint(out_h) == fp_in)
+    del out_h
+
+    value = world * n * K / (elapsed / 1e3) / 1e9
+    ms_per_step = elapsed / K
+    peak, peak_src = peak_hbm()
+
+    # roofline of the dominant kernel (the stable deal, k_scatter)
+    smax = max(phase_ms[f"scatter{j}"] for j in range(4))
+    sc = [phase_ms[f"scatter{j}"] for j in range(4) if phase_ms[f"scatter{j}"] > 0.05 * smax]
+    dominant = max(phase_ms, key=lambda k: phase_ms[k])
+    pass_bytes = n * 2 * (kb + vb)
+    sc_ms = statistics.mean(sc) if sc else None
+    achieved = pass_bytes / (sc_ms / 1e3) / 1e9 if sc_ms else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        traffic = tj.get(f"{args.case}:{n}:k_scatter")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": "k_scatter (one stable deal)", "achieved": achieved,
+                "peak": peak, "unit": "GB/s", "frac": achieved / peak if achieved else None,
+                "traffic": traffic, "algorithmic_bytes_per_launch": pass_bytes,
+                "avg_launch_ms": sc_ms, "launches_per_step": len(sc), "peak_source": peak_src,
+                "largest_phase": dominant}
+    sort_bytes = n * (SORT_BYTES_PER_KEY_U64 if kb == 8 else 0)
+    sort_roof = None
+    if kb == 8 and not c.pairs:
+        gbs = sort_bytes / (ms_per_step / 1e3) / 1e9 / 1.0
+        sort_roof = {"bytes_per_key": SORT_BYTES_PER_KEY_U64, "achieved_GBps": gbs,
+                     "frac_of_measured_copy": gbs / peak, "frac_of_8TBps": gbs / NOMINAL_HBM_GBS}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": c.key_dtype, "data": "synthetic",
+            "config": config_dict(args.case, n, c, desc), "verified": verified,
+            "roofline": roofline, "sort_roofline": sort_roof,
+            "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
+            "gpu_launches": int(launches), "clocks": clk.summary()}
+
+    if not args.quick:
+        line["e2e"] = run_e2e(args, dfr, torch, dev, keys_h, vals_h, tdt, n, kb, vb, world)
+        if rank == 0 and world == 1:
+            line["cpu_baseline"] = run_cpu_baseline(args)
+    if rank == 0:
+        emit(line, args)
+
+
+def run_e2e(args, dfr, torch, dev, keys_h, vals_h, tdt, n, kb, vb, world):
+    """Same metric through the public API with HOST buffers: pinned H2D of the
+    step's input, the sort, D2H of the sorted result, all inside the timing."""
+    import torch.distributed as dist
+    hk = torch.from_numpy(keys_h.view(np.int64 if kb == 8 else np.int32)).pin_memory()
+    ho = torch.empty_like(hk).pin_memory()
+    hv = torch.from_numpy(vals_h.view(np.int32)).pin_memory() if vals_h is not None else None
+    hvo = torch.empty_like(hv).pin_memory() if hv is not None else None
+    dk = torch.empty(n, dtype=tdt, device=dev)
+    dv = torch.empty(n, dtype=torch.int32, device=dev) if hv is not None else None
+    s = torch.cuda.current_stream()
+
+    def step():
+        dk.copy_(hk, non_blocking=True)
+        if dv is not None:
+            dv.copy_(hv, non_blocking=True)
+        dfr.sort(dk, dv)
+        ho.copy_(dk, non_blocking=True)
+        if dv is not None:
+            hvo.copy_(dv, non_blocking=True)
+
+    for _ in range(min(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    K = args.steps
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    a.record(s)
+    for _ in range(K):
+        step()
+    b.record(s)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": world * n * K / (ms / 1e3) / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": n * (kb + vb), "d2h_bytes_per_step": n * (kb + vb),
+            "ms_per_step": ms / K}
+
+
+def run_cpu_baseline(args):
+    import datagen
+    import oracle
+    c, n, _ = workload(args.case, args.n)
+    sample = min(n, 1 << 26)
+    keys, vals = datagen.make_case(args.case, n)
+    keys = keys[:sample].copy()
+    vals = vals[:sample].copy() if vals is not None else None
+    t0 = time.perf_counter()
+    oracle.dfr_sort(keys, vals, copy=False)
+    dt = time.perf_counter() - t0
+    return {"value": sample / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {sample} keys of the {args.case} recipe, one oracle.dfr_sort "
+                      f"call (1 thread, scratch allocation inside the timing), {dt:.1f} s",
+            "host_cpus": os.cpu_count()}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "dfr":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_dfr(args, rank, world, local_rank)
+    if world > 1 and args.impl == "dfr":
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

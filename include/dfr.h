@@ -61,7 +61,22 @@ typedef struct dfr_config {
                                    one non-empty bin — the identity permutation
                                    ("skipping unneeded passes"); 0: run every
                                    pass as Alg. 4 l.6 writes it.  Output identical. */
+  void* const* phase_events; /* NULL, or 2*DFR_NUM_PHASES cudaEvent_t handles created by the
+                                caller: events[2i] / events[2i+1] are recorded on `stream`
+                                before / after phase i (see DFR_PHASE_*); a phase that does
+                                not run records both back to back.  No synchronisation. */
 } dfr_config;
+
+/* Phases timed through dfr_config.phase_events. */
+enum {
+  DFR_PHASE_HIST = 0,     /* k_init + k_hist: one read, p digit histograms (Alg. 4 l.4-5) */
+  DFR_PHASE_PLAN = 1,     /* counts -> bucket offsets */
+  DFR_PHASE_SCATTER0 = 2, /* stable deal of group pass j at DFR_PHASE_SCATTER0 + j, j < 4 */
+  DFR_PHASE_DIVERT = 6,   /* scan for large buckets + small-bucket sort (Alg. 4 l.7-14) */
+  DFR_PHASE_LEVELS = 7,   /* recursion levels >= 1 (Alg. 4 l.11) */
+  DFR_PHASE_MID = 8,      /* buckets N_d < s <= 4096 finished on-chip */
+  DFR_NUM_PHASES = 9
+};
 
 /* Optional device-side counters, read back (with a stream sync) by _ex. */
 typedef struct dfr_stats {
@@ -71,7 +86,7 @@ typedef struct dfr_stats {
   uint64_t mid_buckets;       /* buckets N_d < s <= 4096 finished on-chip (all levels) */
   uint64_t global_segments;   /* buckets > 4096 recursed through the global queue */
   uint32_t levels;            /* recursion levels executed after level 0 */
-  uint32_t reserved;
+  uint32_t overflow;          /* device queue overflow flags (0 = none; non-zero = bug) */
 } dfr_stats;
 
 /*
@@ -125,6 +140,9 @@ int dfr_top_passes(size_t n, int key_bytes, uint32_t n_d);
 
 /* Bytes of scratch one call allocates for n elements of the given widths. */
 size_t dfr_workspace_bytes(size_t n, int key_bytes, int val_bytes);
+
+/* Total kernel launches issued by this library in this process (monotonic). */
+uint64_t dfr_launch_counter(void);
 
 /* Static string for a status code. */
 const char* dfr_status_string(int status);

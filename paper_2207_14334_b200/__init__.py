@@ -19,7 +19,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdfr.so")
+LIB_PATH = os.environ.get("DFR_LIB") or os.path.join(_HERE, "libdfr.so")
 
 # every symbol include/dfr.h declares
 EXPORTS = (
@@ -27,8 +27,10 @@ EXPORTS = (
     "dfr_sort_u32_ex", "dfr_sort_u64_ex", "dfr_sort_pairs_u32_ex",
     "dfr_histogram_u32", "dfr_histogram_u64",
     "dfr_partition_pass_u64", "dfr_partition_pass_pairs_u32",
-    "dfr_top_passes", "dfr_workspace_bytes", "dfr_status_string",
+    "dfr_top_passes", "dfr_workspace_bytes", "dfr_launch_counter", "dfr_status_string",
 )
+
+PHASES = ("hist", "plan", "scatter0", "scatter1", "scatter2", "scatter3", "divert", "levels", "mid")
 
 DFR_OK, DFR_ERR_INVALID, DFR_ERR_ALLOC, DFR_ERR_CUDA, DFR_ERR_TOO_LARGE = 0, -1, -2, -3, -4
 
@@ -38,14 +40,15 @@ class DfrError(RuntimeError):
 
 
 class Config(ctypes.Structure):
-    _fields_ = [("n_d", ctypes.c_uint32), ("skip_trivial_passes", ctypes.c_uint32)]
+    _fields_ = [("n_d", ctypes.c_uint32), ("skip_trivial_passes", ctypes.c_uint32),
+                ("phase_events", ctypes.POINTER(ctypes.c_void_p))]
 
 
 class Stats(ctypes.Structure):
     _fields_ = [("level0_p", ctypes.c_uint32), ("level0_passes_run", ctypes.c_uint32),
                 ("level0_large", ctypes.c_uint64), ("mid_buckets", ctypes.c_uint64),
                 ("global_segments", ctypes.c_uint64), ("levels", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32)]
+                ("overflow", ctypes.c_uint32)]
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f, _ in self._fields_}
@@ -78,6 +81,7 @@ def lib() -> ctypes.CDLL:
         "dfr_top_passes": [sz, i32, u32],
         "dfr_workspace_bytes": [sz, i32, i32],
         "dfr_status_string": [i32],
+        "dfr_launch_counter": [],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -85,6 +89,7 @@ def lib() -> ctypes.CDLL:
         f.restype = i32
     L.dfr_workspace_bytes.restype = ctypes.c_size_t
     L.dfr_status_string.restype = ctypes.c_char_p
+    L.dfr_launch_counter.restype = ctypes.c_uint64
     _lib = L
     return L
 
@@ -116,35 +121,46 @@ def _dev_tensor(t, widths):
     return t
 
 
-def _cfg(n_d, skip_trivial):
-    return Config(int(n_d), 1 if skip_trivial else 0)
+def _cfg(n_d, skip_trivial, events=None):
+    """events: None or a sequence of 2*len(PHASES) torch.cuda.Event(enable_timing=True)."""
+    c = Config(int(n_d), 1 if skip_trivial else 0, None)
+    if events is not None:
+        arr = (ctypes.c_void_p * len(events))(*[int(e.cuda_event) for e in events])
+        c._keep = arr
+        c.phase_events = ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
+    return c
 
 
-def sort_u32(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False):
+def launch_counter() -> int:
+    return int(lib().dfr_launch_counter())
+
+
+def sort_u32(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, events=None):
     """In-place ascending sort of a contiguous CUDA tensor of 32-bit keys (bit
     patterns read as uint32)."""
     _dev_tensor(keys, (4,))
     st = Stats() if stats else None
     rc = lib().dfr_sort_u32_ex(keys.data_ptr(), keys.numel(), _stream(stream),
-                               ctypes.byref(_cfg(n_d, skip_trivial)),
+                               ctypes.byref(_cfg(n_d, skip_trivial, events)),
                                ctypes.byref(st) if st is not None else None)
     _check(rc, "dfr_sort_u32")
     return st.as_dict() if st is not None else None
 
 
-def sort_u64(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False):
+def sort_u64(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, events=None):
     """In-place ascending sort of a contiguous CUDA tensor of 64-bit keys (bit
     patterns read as uint64; int64 tensors are accepted as raw storage)."""
     _dev_tensor(keys, (8,))
     st = Stats() if stats else None
     rc = lib().dfr_sort_u64_ex(keys.data_ptr(), keys.numel(), _stream(stream),
-                               ctypes.byref(_cfg(n_d, skip_trivial)),
+                               ctypes.byref(_cfg(n_d, skip_trivial, events)),
                                ctypes.byref(st) if st is not None else None)
     _check(rc, "dfr_sort_u64")
     return st.as_dict() if st is not None else None
 
 
-def sort_pairs_u32(keys, vals, *, n_d=64, skip_trivial=True, stream=None, stats=False):
+def sort_pairs_u32(keys, vals, *, n_d=64, skip_trivial=True, stream=None, stats=False,
+                   events=None):
     """Stable in-place sort of (uint32 key, uint32 value) pairs held in two
     contiguous CUDA tensors of equal length."""
     _dev_tensor(keys, (4,))
@@ -153,7 +169,7 @@ def sort_pairs_u32(keys, vals, *, n_d=64, skip_trivial=True, stream=None, stats=
         raise DfrError("keys and vals differ in length")
     st = Stats() if stats else None
     rc = lib().dfr_sort_pairs_u32_ex(keys.data_ptr(), vals.data_ptr(), keys.numel(),
-                                     _stream(stream), ctypes.byref(_cfg(n_d, skip_trivial)),
+                                     _stream(stream), ctypes.byref(_cfg(n_d, skip_trivial, events)),
                                      ctypes.byref(st) if st is not None else None)
     _check(rc, "dfr_sort_pairs_u32")
     return st.as_dict() if st is not None else None

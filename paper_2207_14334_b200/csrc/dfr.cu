@@ -16,6 +16,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include "dfr.h"
@@ -84,19 +85,19 @@ __global__ void __launch_bounds__(THREADS) k_plan2(const __grid_constant__ Param
 }
 
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(THREADS) k_scatter(const __grid_constant__ Params<K> P, int j) {
+__global__ void __launch_bounds__(THREADS, 3) k_scatter(const __grid_constant__ Params<K> P, int j) {
   extern __shared__ __align__(16) uint32_t sm[];
   Phases<K, PAIRS>::scatter(P, j, sm);
 }
 
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(THREADS) k_divert(const __grid_constant__ Params<K> P) {
+__global__ void __launch_bounds__(THREADS, 4) k_divert(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
   Phases<K, PAIRS>::divert(P, sm);
 }
 
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(THREADS) k_mid(const __grid_constant__ Params<K> P) {
+__global__ void __launch_bounds__(THREADS, 2) k_mid(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
   Phases<K, PAIRS>::mid(P, sm);
 }
@@ -142,6 +143,36 @@ __global__ void k_seed_mid(Params<K> P, uint32_t n) {
 }
 
 // ------------------------------------------------------------------ host
+static std::atomic<unsigned long long> g_launches{0};
+
+#ifdef DFR_DEBUG
+#define DFR_CHECK_LAUNCH(name)                                                          \
+  do {                                                                                  \
+    cudaError_t e_ = cudaStreamSynchronize(st);                                          \
+    if (e_ == cudaSuccess) e_ = cudaGetLastError();                                      \
+    fprintf(stderr, "[dfr debug] %s: %s\n", name, cudaGetErrorString(e_));               \
+  } while (0)
+#else
+#define DFR_CHECK_LAUNCH(name) \
+  do {                         \
+  } while (0)
+#endif
+
+struct PhaseEv {  // optional caller-provided events around each phase
+  void* const* ev;
+  cudaStream_t st;
+  void begin(int i) const {
+    if (ev && ev[2 * i]) cudaEventRecord((cudaEvent_t)ev[2 * i], st);
+  }
+  void end(int i) const {
+    if (ev && ev[2 * i + 1]) cudaEventRecord((cudaEvent_t)ev[2 * i + 1], st);
+  }
+  void skip(int i) const {
+    begin(i);
+    end(i);
+  }
+};
+
 struct Dev {
   int sms = 0;
   int occ_hist = 0, occ_scatter = 0, occ_divert = 0, occ_mid = 0, occ_levels = 0;
@@ -160,6 +191,14 @@ static cudaError_t get_dev(Dev& out) {
   std::call_once(once[dev], [&]() {
     Dev d;
     cudaError_t err = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    // keep freed scratch cached in the stream-ordered pool: every call allocates
+    // and frees its workspace (the paper times allocation), which must
+    // then cost microseconds, not a re-map of gigabytes
+    cudaMemPool_t pool;
+    if (err == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      unsigned long long thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     auto setup = [&](const void* f, size_t smem, int* occ) {
       if (err != cudaSuccess) return;
       err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -280,35 +319,57 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
   Params<K> P = make_params<K>(ws, L, keys, vals, PAIRS, n_d, skip);
   const uint32_t nn = (uint32_t)n;
   const int sms = dv.sms;
+  const PhaseEv pe{cfg ? cfg->phase_events : nullptr, st};
 
   if (n <= (size_t)MID_CAP) {  // the whole input fits one on-chip DFR
+    for (int i = 0; i < DFR_PHASE_MID; ++i) pe.skip(i);
+    pe.begin(DFR_PHASE_MID);
     k_seed_mid<K, PAIRS><<<1, 1, 0, st>>>(P, nn);
     k_mid<K, PAIRS><<<1, THREADS, Ph::SMEM_MID, st>>>(P);
+    pe.end(DFR_PHASE_MID);
+    g_launches += 2;
   } else {
     int p0 = est_top_passes(n, n_d);
     if (p0 > (int)sizeof(K)) p0 = (int)sizeof(K);
     const uint32_t tiles = (nn + TILE - 1) / TILE;
+    pe.begin(DFR_PHASE_HIST);
     k_init<K, PAIRS><<<1, THREADS, 64, st>>>(P, nn);
     const int g_hist = (int)std::min<uint32_t>(tiles, (uint32_t)(sms * std::max(1, dv.occ_hist)));
     k_hist<K, PAIRS><<<g_hist, THREADS, Ph::SMEM_HIST, st>>>(P);
+    pe.end(DFR_PHASE_HIST);
+    pe.begin(DFR_PHASE_PLAN);
     k_plan2<K, PAIRS><<<1, THREADS, 64, st>>>(P);
+    pe.end(DFR_PHASE_PLAN);
     const int g_sc = (int)std::min<uint32_t>(tiles, (uint32_t)(sms * std::max(1, dv.occ_scatter)));
-    for (int j = 0; j < p0; ++j) k_scatter<K, PAIRS><<<g_sc, THREADS, Ph::SMEM_SCATTER, st>>>(P, j);
+    for (int j = 0; j < MAX_PASSES; ++j) {
+      if (j >= p0) {
+        pe.skip(DFR_PHASE_SCATTER0 + j);
+        continue;
+      }
+      pe.begin(DFR_PHASE_SCATTER0 + j);
+      k_scatter<K, PAIRS><<<g_sc, THREADS, Ph::SMEM_SCATTER, st>>>(P, j);
+      pe.end(DFR_PHASE_SCATTER0 + j);
+    }
     const uint32_t chunks = (nn + P.chunk - 1) / P.chunk;
     const int g_dv = (int)std::min<uint32_t>(chunks, (uint32_t)(sms * std::max(1, dv.occ_divert)));
+    pe.begin(DFR_PHASE_DIVERT);
     k_divert<K, PAIRS><<<g_dv, THREADS, Ph::SMEM_DIVERT, st>>>(P);
-    if (n > (size_t)MID_CAP) {
-      void* args[] = {&P};
-      const int g_lv = sms * std::max(1, dv.occ_levels);
-      cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_levels<K, PAIRS>, g_lv, THREADS,
-                                                  args, Ph::SMEM_LEVEL, st);
-      if (e != cudaSuccess) {
-        cudaFreeAsync(ws, st);
-        return DFR_ERR_CUDA;
-      }
+    pe.end(DFR_PHASE_DIVERT);
+    pe.begin(DFR_PHASE_LEVELS);
+    void* args[] = {&P};
+    const int g_lv = sms * std::max(1, dv.occ_levels);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_levels<K, PAIRS>, g_lv, THREADS,
+                                                args, Ph::SMEM_LEVEL, st);
+    pe.end(DFR_PHASE_LEVELS);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(ws, st);
+      return DFR_ERR_CUDA;
     }
+    pe.begin(DFR_PHASE_MID);
     const int g_mid = sms * std::max(1, dv.occ_mid);
     k_mid<K, PAIRS><<<g_mid, THREADS, Ph::SMEM_MID, st>>>(P);
+    pe.end(DFR_PHASE_MID);
+    g_launches += 6 + p0;
   }
   cudaError_t e = cudaGetLastError();
   int rc = (e == cudaSuccess) ? DFR_OK : DFR_ERR_CUDA;
@@ -324,7 +385,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
       stats->mid_buckets = h.mid_buckets;
       stats->global_segments = h.global_segments;
       stats->levels = h.levels_run;
-      stats->reserved = h.overflow;
+      stats->overflow = h.overflow;
     }
   }
   if (cudaFreeAsync(ws, st) != cudaSuccess && rc == DFR_OK) rc = DFR_ERR_CUDA;
@@ -355,14 +416,19 @@ static int stage_impl(const K* in, const uint32_t* vin, K* out, uint32_t* vout, 
   const uint32_t nn = (uint32_t)n;
   const uint32_t tiles = (nn + TILE - 1) / TILE;
   k_init_stage<K, PAIRS><<<1, THREADS, 0, st>>>(P, nn, digit_lo, p);
+  DFR_CHECK_LAUNCH("k_init_stage");
+  g_launches += d_counts ? 2 : 4;
   const int g_hist = (int)std::min<uint32_t>(tiles, (uint32_t)(dv.sms * std::max(1, dv.occ_hist)));
   k_hist<K, PAIRS><<<g_hist, THREADS, Ph::SMEM_HIST, st>>>(P);
+  DFR_CHECK_LAUNCH("k_hist(stage)");
   if (d_counts) {
     cudaMemcpyAsync(d_counts, P.hist, (size_t)p * 256 * 4, cudaMemcpyDeviceToDevice, st);
   } else {
     k_plan2<K, PAIRS><<<1, THREADS, 64, st>>>(P);
+    DFR_CHECK_LAUNCH("k_plan2(stage)");
     const int g_sc = (int)std::min<uint32_t>(tiles, (uint32_t)(dv.sms * std::max(1, dv.occ_scatter)));
     k_scatter<K, PAIRS><<<g_sc, THREADS, Ph::SMEM_SCATTER, st>>>(P, 0);
+    DFR_CHECK_LAUNCH("k_scatter(stage)");
   }
   cudaError_t e = cudaGetLastError();
   cudaFreeAsync(ws, st);
@@ -429,6 +495,8 @@ int dfr_partition_pass_pairs_u32(const uint32_t* d_keys_in, const uint32_t* d_va
   return dfr::stage_impl<uint32_t, false>(d_keys_in, nullptr, d_keys_out, nullptr, n, d, 1,
                                           nullptr, (cudaStream_t)stream);
 }
+
+uint64_t dfr_launch_counter(void) { return dfr::g_launches.load(); }
 
 int dfr_top_passes(size_t n, int key_bytes, uint32_t n_d) {
   if (n_d == 0) n_d = DFR_DEFAULT_ND;

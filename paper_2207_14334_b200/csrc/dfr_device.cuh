@@ -115,6 +115,47 @@ __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// ---- TMA bulk copies (cp.async.bulk) + mbarrier ---------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// one thread: expect `bytes` and launch a 1-D bulk copy global -> shared
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void red_add_shared(uint32_t saddr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+
 // least p >= 0 with len <= n_d * 256^p  (Alg. 4 l.4; reading S:284)
 __host__ __device__ __forceinline__ int est_top_passes(uint64_t len, uint32_t n_d) {
   int p = 0;
@@ -163,27 +204,34 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
 }
 
 // Warp-level multi-split rank (stable): items are (j, lane) in j-major order;
-// rank[j] = number of earlier items of this warp with the same digit.
-// whist (256 u32 for this warp, zeroed) accumulates the warp's digit counts.
-// Digits >= 256 mark invalid items (not counted).
-template <int N>
-__device__ __forceinline__ void warp_rank(const uint32_t (&dig)[N], uint32_t (&rank)[N],
-                                          uint32_t* whist) {
+// the rank of an item = number of earlier items of this warp with the same
+// digit.  The peers of a lane (lanes holding the same digit in this step) are
+// found with 8 ballots, one per digit bit — vote/ALU work only: MATCH.ANY costs
+// ~64 SM cycles per instruction on sm_100a, and a shared-memory match spends
+// the shared-memory pipe, which is this kernel's bottleneck.  The lowest peer
+// advances the warp's running count of the digit with one atomicAdd and
+// broadcasts the old value.  whist (256 u32) must be zero on entry.
+// io[j]: in = digit (256 marks an invalid item, only when !FULL);
+// out = digit | rank << 16.
+template <int N, bool FULL>
+__device__ __forceinline__ void warp_rank(uint32_t (&io)[N], uint32_t* whist) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int j = 0; j < N; ++j) {
-    const uint32_t d = dig[j];
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t leader = __ffs(peers) - 1;
-    uint32_t base = 0;
-    if (lane == leader && d < 256) {
-      base = whist[d];
-      whist[d] = base + __popc(peers);
+    const uint32_t d = io[j];
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < (FULL ? 8 : 9); ++b) {
+      const bool set = (d >> b) & 1u;
+      const uint32_t v = __ballot_sync(0xffffffffu, set);
+      peers &= set ? v : ~v;
     }
-    base = __shfl_sync(0xffffffffu, base, leader);
-    rank[j] = base + __popc(peers & lt);
-    __syncwarp();
+    const uint32_t leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (lane == leader && (FULL || d < 256)) old = atomicAdd(&whist[d], __popc(peers));
+    old = __shfl_sync(0xffffffffu, old, leader);
+    io[j] = d | ((old + __popc(peers & lt)) << 16);
   }
 }
 

@@ -32,13 +32,14 @@ struct Phases {
   static constexpr int CT_BITS = 8 * sizeof(CT);
 
   // ------------------------------------------------------------ smem sizes
-  static constexpr size_t SMEM_HIST = MAX_PASSES * 256 * 4 + 64;
+  static constexpr size_t SMEM_HIST = WARPS * MAX_PASSES * 256 * 4 + 64;
+  static constexpr int SCATTER_HDR_WORDS = WARPS * 256 + 256 * 2 + 32;
   static constexpr size_t SMEM_SCATTER =
-      WARPS * 256 * 4 + 256 * 4 * 2 + 64 + TILE * sizeof(K) + (PAIRS ? TILE * 4 : 0);
+      SCATTER_HDR_WORDS * 4 + TILE * sizeof(K) + (PAIRS ? TILE * 4 : 0);
   static constexpr size_t SMEM_DIVERT =
-      WIN * sizeof(K) + WIN * sizeof(CT) + (PAIRS ? WIN * 4 : 0) + (WIN / 32 + 8) * 4 + 64;
+      WIN * sizeof(K) + (WIN + 8) * 4 + WIN * 4 + (PAIRS ? WIN * 4 : 0) + (WIN / 32 + 16) * 4;
   static constexpr size_t SMEM_MID = 2 * MID_CAP * sizeof(K) + (PAIRS ? 2 * MID_CAP * 4 : 0) +
-                                     MID_CAP * sizeof(CT) + WARPS * 256 * 4 + 256 * 4 +
+                                     (MID_CAP + 8) * sizeof(CT) + 3 * WARPS * 256 * 4 + 256 * 4 +
                                      (MID_CAP / 32 + 8) * 4 + 512 * 8 + 128;
   static constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
   static constexpr size_t SMEM_LEVEL =
@@ -135,9 +136,13 @@ struct Phases {
                                     uint32_t* sh, unsigned long long diff) {
     __syncthreads();
     for (uint32_t j = 0; j < s.p; ++j) {
-      uint32_t v = sh[j * 256 + threadIdx.x];
+      uint32_t v = 0;
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) {
+        v += sh[(w * MAX_PASSES + j) * 256 + threadIdx.x];
+        sh[(w * MAX_PASSES + j) * 256 + threadIdx.x] = 0;
+      }
       if (v) atomicAdd(&P.hist[(size_t)(s.hist_off + j) * 256 + threadIdx.x], v);
-      sh[j * 256 + threadIdx.x] = 0;
     }
     // diff: warp OR then one atomic per warp
     unsigned long long d = diff;
@@ -147,15 +152,73 @@ struct Phases {
     __syncthreads();
   }
 
-  static __device__ __forceinline__ void count_key(uint32_t* sh, K k, bool valid, int low,
-                                                   uint32_t p) {
+  // warp-private sub-histograms (no cross-warp contention).  A warp whose 32
+  // keys share the whole group prefix (sorted, skewed, constant inputs) adds
+  // 32 once per digit; otherwise each lane adds 1 to its digit's counter.
+  template <int NP>
+  static __device__ __forceinline__ void count_key(uint32_t shw, K k, bool valid, int low) {
     const uint32_t lane = threadIdx.x & 31;
+    const K pre = k >> (8 * low);
+    const K pre0 = __shfl_sync(0xffffffffu, pre, 0);
+    if (__all_sync(0xffffffffu, valid && pre == pre0)) {
+      if (lane == 0) {
 #pragma unroll
-    for (int j = 0; j < MAX_PASSES; ++j) {
-      if ((uint32_t)j < p) {  // warp-uniform
-        const uint32_t d = valid ? digit_of(k, low + j) : 256u + j;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        if (valid && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&sh[j * 256 + d], __popc(peers));
+        for (int j = 0; j < NP; ++j) red_add_shared(shw + 4 * (j * 256 + digit_of(k, low + j)), 32u);
+      }
+    } else if (valid) {
+#pragma unroll
+      for (int j = 0; j < NP; ++j) red_add_shared(shw + 4 * (j * 256 + digit_of(k, low + j)), 1u);
+    }
+  }
+
+  // one tile: diff mask + counts of the NP group digits
+  template <int NP>
+  static __device__ __forceinline__ void hist_tile(const K* tp, uint32_t cnt, K kref, int low,
+                                                   uint32_t shw, unsigned long long& diff) {
+    if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0) {
+      const uint32_t nv = cnt / VEC;
+      const uint4* vp = reinterpret_cast<const uint4*>(tp);
+      constexpr int U = 4;  // 4 independent 16-byte loads in flight per thread
+      uint32_t vb = 0;
+      for (; vb + U * THREADS <= nv; vb += U * THREADS) {  // full blocks: no bounds checks
+        uint4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = __ldg(vp + vb + u * THREADS + threadIdx.x);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const K* kk = reinterpret_cast<const K*>(&x[u]);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            diff |= (unsigned long long)(kk[e] ^ kref);
+            count_key<NP>(shw, kk[e], true, low);
+          }
+        }
+      }
+      for (; vb < nv; vb += THREADS) {
+        const uint32_t v = vb + threadIdx.x;
+        const bool ok = v < nv;
+        uint4 x = ok ? __ldg(vp + v) : make_uint4(0, 0, 0, 0);
+        const K* kk = reinterpret_cast<const K*>(&x);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          if (ok) diff |= (unsigned long long)(kk[e] ^ kref);
+          count_key<NP>(shw, kk[e], ok, low);
+        }
+      }
+      if (nv * VEC < cnt && threadIdx.x < 32) {  // < VEC leftover keys, warp 0
+        const uint32_t ii = nv * VEC + threadIdx.x;
+        const bool ok = ii < cnt;
+        K k = ok ? tp[ii] : K(0);
+        if (ok) diff |= (unsigned long long)(k ^ kref);
+        count_key<NP>(shw, k, ok, low);
+      }
+    } else {
+      for (uint32_t ib = 0; ib < cnt; ib += THREADS) {
+        const uint32_t i = ib + threadIdx.x;
+        const bool ok = i < cnt;
+        K k = ok ? tp[i] : K(0);
+        if (ok) diff |= (unsigned long long)(k ^ kref);
+        count_key<NP>(shw, k, ok, low);
       }
     }
   }
@@ -173,8 +236,9 @@ struct Phases {
     const uint32_t t0 = blockIdx.x * per;
     const uint32_t t1 = min(total, t0 + per);
     if (t0 >= t1) return;
-    uint32_t* sh = sm;
-    for (int j = 0; j < MAX_PASSES; ++j) sh[j * 256 + threadIdx.x] = 0;
+    uint32_t* sh = sm;  // [WARPS][MAX_PASSES][256]
+    const uint32_t shw = smem_u32(sh + (threadIdx.x >> 5) * MAX_PASSES * 256);
+    for (int j = 0; j < WARPS * MAX_PASSES; ++j) sh[j * 256 + threadIdx.x] = 0;
     uint32_t si = upper_index(nseg, t0, [&](uint32_t i) { return q[i].tile0; });
     Seg s = q[si];
     unsigned long long diff = 0;
@@ -194,35 +258,11 @@ struct Phases {
       const K* src = s.buf ? P.B : P.A;
       const K kref = src[s.start];
       const K* tp = src + base;
-      if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0) {
-        const uint32_t nv = cnt / VEC;
-        const uint4* vp = reinterpret_cast<const uint4*>(tp);
-        for (uint32_t vb = 0; vb < nv; vb += THREADS) {
-          const uint32_t v = vb + threadIdx.x;
-          const bool ok = v < nv;
-          uint4 x = ok ? __ldg(vp + v) : make_uint4(0, 0, 0, 0);
-          const K* kk = reinterpret_cast<const K*>(&x);
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            if (ok) diff |= (unsigned long long)(kk[e] ^ kref);
-            count_key(sh, kk[e], ok, s.low, s.p);
-          }
-        }
-        for (uint32_t i = nv * VEC; i < cnt; i += THREADS) {  // < VEC keys, warp 0
-          const uint32_t ii = i + threadIdx.x;
-          const bool ok = ii < cnt;
-          K k = ok ? tp[ii] : K(0);
-          if (ok) diff |= (unsigned long long)(k ^ kref);
-          if (threadIdx.x < 32) count_key(sh, k, ok, s.low, s.p);
-        }
-      } else {
-        for (uint32_t ib = 0; ib < cnt; ib += THREADS) {
-          const uint32_t i = ib + threadIdx.x;
-          const bool ok = i < cnt;
-          K k = ok ? tp[i] : K(0);
-          if (ok) diff |= (unsigned long long)(k ^ kref);
-          count_key(sh, k, ok, s.low, s.p);
-        }
+      switch (s.p) {
+        case 1: hist_tile<1>(tp, cnt, kref, s.low, shw, diff); break;
+        case 2: hist_tile<2>(tp, cnt, kref, s.low, shw, diff); break;
+        case 3: hist_tile<3>(tp, cnt, kref, s.low, shw, diff); break;
+        default: hist_tile<4>(tp, cnt, kref, s.low, shw, diff); break;
       }
     }
     hist_flush(P, q, si, s, sh, diff);
@@ -287,142 +327,211 @@ struct Phases {
   }
 
   // ------------------------------------------------------------- scatter
-  // One stable deal on group digit low+j for every active segment.  Tiles of
-  // TILE keys are claimed by dynamic tickets; each tile ranks its keys with a
-  // warp-level multi-split (match_any), publishes its per-digit aggregate,
-  // resolves its exclusive per-digit prefix by decoupled look-back over the
-  // preceding tiles of the same segment, reorders the tile through shared
-  // memory by digit and writes each digit run contiguously.
+  // One stable deal on group digit low+j for every active segment.  A
+  // persistent CTA claims a tile of TILE keys by dynamic ticket (forward
+  // progress for the look-back), pulls it into shared memory with one TMA bulk
+  // copy, ranks it with the warp-level multi-split, publishes its per-digit
+  // aggregate, resolves its exclusive per-digit prefix by decoupled look-back
+  // over the segment's earlier tiles, reorders the tile by digit in shared
+  // memory and writes every digit run contiguously.
+  static __device__ __forceinline__ bool pass_active(const Seg& s, int j) {
+    return (uint32_t)j < s.p && !((s.flags >> j) & 1u) &&
+           !(s.flags & (SEG_SKIP_DIVERT | SEG_COPY | SEG_DONE));
+  }
+  static __device__ __forceinline__ uint32_t src_buf(const Seg& s, int j) {
+    const uint32_t before = (uint32_t)j - __popc(s.flags & ((1u << j) - 1u));
+    return s.buf ^ (before & 1u);
+  }
+
+  // rank, publish, reorder, look back, write out — one staged tile
+  template <bool FULL>
+  static __device__ __forceinline__ void deal_tile(const Params<K>& P, const Seg& s, int j,
+                                                   uint32_t t, uint32_t lt, uint32_t cnt, int dg,
+                                                   uint32_t* status, K* sk, V* sv, uint32_t* whist,
+                                                   uint32_t* mywh, int* s_dst,
+                                                   uint32_t* s_lstart, uint32_t* s_warp, K* dst,
+                                                   V* dstv) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // warp-striped items: (jj, lane) -> w*32*KPT + jj*32 + lane
+    K key[KPT];
+    V val[KPT];
+    uint32_t dr[KPT];
+#pragma unroll
+    for (int jj = 0; jj < KPT; ++jj) {
+      const uint32_t idx = w * 32 * KPT + jj * 32 + lane;
+      key[jj] = sk[idx];
+      if (PAIRS) val[jj] = sv[idx];
+      dr[jj] = (FULL || idx < cnt) ? digit_of(key[jj], dg) : 256u;
+    }
+    warp_rank<KPT, FULL>(dr, mywh);
+    __syncthreads();
+    // per digit: exclusive offsets of each warp, tile aggregate -> publish
+    const uint32_t dd = threadIdx.x;
+    uint32_t run = 0;
+#pragma unroll
+    for (int e = 0; e < WARPS; ++e) {
+      const uint32_t x = whist[e * 256 + dd];
+      whist[e * 256 + dd] = run;
+      run += x;
+    }
+    uint32_t* my_status = status + (size_t)t * 256 + dd;
+    st_relaxed(my_status, (lt == 0 ? FLAG_INC : FLAG_AGG) | run);
+    uint32_t tot;
+    const uint32_t lstart = block_excl_scan(run, s_warp, &tot);
+#pragma unroll
+    for (int e = 0; e < WARPS; ++e) whist[e * 256 + dd] += lstart;  // warp base in the tile
+    __syncthreads();
+    // reorder the tile by digit in shared memory (stable); this only needs the
+    // local offsets, so it runs before the look-back and gives the preceding
+    // tiles time to publish
+#pragma unroll
+    for (int jj = 0; jj < KPT; ++jj) {
+      const uint32_t dgt = dr[jj] & 0xffffu;
+      if (FULL || dgt < 256) {
+        const uint32_t pos = mywh[dgt] + (dr[jj] >> 16);
+        sk[pos] = key[jj];
+        if (PAIRS) sv[pos] = val[jj];
+      }
+    }
+    uint32_t excl = 0;
+    if (lt > 0) {  // decoupled look-back, up to 4 predecessors per round trip
+      int tt = (int)t - 1;
+      const int t0 = (int)s.tile0;  // publishes FLAG_INC, so the walk ends there
+      while (true) {
+        uint32_t v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          v[k] = (tt - k >= t0) ? ld_relaxed(status + (size_t)(tt - k) * 256 + dd) : FLAG_INC;
+        int k = 0;
+        bool done = false;
+#pragma unroll
+        for (; k < 4; ++k) {
+          if ((v[k] >> 30) == 0) break;  // not published yet: retry from here
+          excl += v[k] & VAL_MASK;
+          if (v[k] & FLAG_INC) {
+            done = true;
+            break;
+          }
+        }
+        if (done) break;
+        tt -= k;
+      }
+      st_relaxed(my_status, FLAG_INC | (excl + run));
+    }
+    const uint32_t bstart = P.hist[(size_t)(s.hist_off + j) * 256 + dd];
+    s_dst[dd] = (int)(s.start + bstart + excl) - (int)lstart;
+    __syncthreads();
+    // coalesced write of each digit run
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < (FULL ? (uint32_t)TILE : cnt); i += THREADS) {
+      const K k = sk[i];
+      const int o = s_dst[digit_of(k, dg)] + (int)i;
+#ifdef DFR_DEBUG
+      if (o < (int)s.start || o >= (int)(s.start + s.len)) {
+        printf("scatter OOB: t=%u i=%u o=%d seg=[%u,%u)\n", t, i, o, s.start, s.start + s.len);
+        __trap();
+      }
+#endif
+      dst[o] = k;
+      if (PAIRS) dstv[o] = sv[i];
+    }
+  }
+
   static __device__ void scatter(const Params<K>& P, int j, uint32_t* sm) {
     Ctl* c = P.ctl;
     const uint32_t total = c->total_tiles, nseg = c->nseg;
     if ((uint32_t)j >= c->max_p) return;  // no segment of this level has pass j
-    Seg* q = P.segq[c->cur];
-    uint32_t* whist = sm;                                   // WARPS*256
-    int* s_dst = reinterpret_cast<int*>(whist + WARPS * 256);  // 256
+    const Seg* q = P.segq[c->cur];
+    uint32_t* whist = sm;                                       // WARPS*256
+    int* s_dst = reinterpret_cast<int*>(whist + WARPS * 256);   // 256
     uint32_t* s_lstart = reinterpret_cast<uint32_t*>(s_dst + 256);  // 256
-    uint32_t* s_misc = s_lstart + 256;                      // 16
-    K* sk = reinterpret_cast<K*>(s_misc + 16);
-    V* sv = reinterpret_cast<V*>(sk + TILE);
+    uint32_t* s_warp = s_lstart + 256;                          // 8
+    uint32_t* s_misc = s_warp + 8;                              // 8: ticket, seg, tma
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(s_misc + 8);  // 8-aligned
+    K* const sk = reinterpret_cast<K*>(sm + SCATTER_HDR_WORDS);
+    V* const sv = reinterpret_cast<V*>(sk + TILE);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     uint32_t* mywh = whist + w * 256;
     uint32_t* status = P.status + (size_t)j * P.status_stride;
+    if (threadIdx.x == 0) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+    }
+    uint32_t parity = 0;
 
     while (true) {
+      __syncthreads();  // previous tile fully written out; s_misc free
       if (threadIdx.x == 0) {
         const uint32_t t = atomicAdd(&c->ticket[j], 1u);
         s_misc[0] = t;
-        s_misc[1] = t < total ? upper_index(nseg, t, [&](uint32_t i) { return q[i].tile0; }) : 0;
+        s_misc[2] = 0;
+        if (t < total) {
+          const uint32_t si = upper_index(nseg, t, [&](uint32_t i) { return q[i].tile0; });
+          s_misc[1] = si;
+          const Seg& s = q[si];
+          const uint32_t lt = t - s.tile0;
+          if (pass_active(s, j) && s.len - lt * TILE >= (uint32_t)TILE) {
+            const uint32_t sb = src_buf(s, j);
+            const K* src = (sb ? P.B : P.A) + s.start + lt * TILE;
+            const V* srcv = PAIRS ? (sb ? P.Bv : P.Av) + s.start + lt * TILE : nullptr;
+            if (!(reinterpret_cast<uintptr_t>(src) & 15) &&
+                !(PAIRS && (reinterpret_cast<uintptr_t>(srcv) & 15))) {
+              fence_proxy_async();
+              const uint32_t bytes = TILE * sizeof(K) + (PAIRS ? TILE * 4 : 0);
+              asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                               smem_u32(bar)),
+                           "r"(bytes)
+                           : "memory");
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+                  "%2, [%3];" ::"r"(smem_u32(sk)),
+                  "l"(src), "r"((uint32_t)(TILE * sizeof(K))), "r"(smem_u32(bar))
+                  : "memory");
+              if (PAIRS)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+                    "%2, [%3];" ::"r"(smem_u32(sv)),
+                    "l"(srcv), "r"((uint32_t)(TILE * 4)), "r"(smem_u32(bar))
+                    : "memory");
+              s_misc[2] = 1;
+            }
+          }
+        }
       }
+#pragma unroll
+      for (int e = 0; e < WARPS; ++e) whist[e * 256 + threadIdx.x] = 0;
       __syncthreads();
       const uint32_t t = s_misc[0];
       if (t >= total) break;
       const Seg s = q[s_misc[1]];
-      if ((uint32_t)j >= s.p || ((s.flags >> j) & 1u) ||
-          (s.flags & (SEG_SKIP_DIVERT | SEG_COPY | SEG_DONE))) {
-        __syncthreads();
-        continue;
-      }
+      if (!pass_active(s, j)) continue;
       const uint32_t lt = t - s.tile0;
       const uint32_t base = s.start + lt * TILE;
       const uint32_t cnt = min((uint32_t)TILE, s.len - lt * TILE);
-      const uint32_t before = (uint32_t)j - __popc(s.flags & ((1u << j) - 1u));
-      const uint32_t sb = s.buf ^ (before & 1u);
+      const uint32_t sb = src_buf(s, j);
       const K* src = sb ? P.B : P.A;
       K* dst = sb ? P.A : P.B;
       const V* srcv = sb ? P.Bv : P.Av;
       V* dstv = sb ? P.Av : P.Bv;
       const int dg = s.low + j;
 
-      // stage the tile in shared memory (16-byte vector loads when aligned)
-      const K* tp = src + base;
-      if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0 && cnt == (uint32_t)TILE) {
-        const uint4* vp = reinterpret_cast<const uint4*>(tp);
-        uint4* sp = reinterpret_cast<uint4*>(sk);
-#pragma unroll 4
-        for (int v = threadIdx.x; v < TILE / VEC; v += THREADS) sp[v] = __ldg(vp + v);
-      } else {
-        for (uint32_t i = threadIdx.x; i < cnt; i += THREADS) sk[i] = tp[i];
+      if (s_misc[2]) {
+        mbar_wait(bar, parity);
+        parity ^= 1u;
+      } else {  // ragged tail / unaligned tile: plain coalesced loads
+        for (uint32_t i = threadIdx.x; i < cnt; i += THREADS) sk[i] = src[base + i];
+        if (PAIRS)
+          for (uint32_t i = threadIdx.x; i < cnt; i += THREADS) sv[i] = srcv[base + i];
+        __syncthreads();
       }
-      if (PAIRS) {
-        const V* vp = srcv + base;
-        if ((reinterpret_cast<uintptr_t>(vp) & 15) == 0 && cnt == (uint32_t)TILE) {
-          const uint4* v4 = reinterpret_cast<const uint4*>(vp);
-          uint4* s4 = reinterpret_cast<uint4*>(sv);
-#pragma unroll 4
-          for (int v = threadIdx.x; v < TILE / 4; v += THREADS) s4[v] = __ldg(v4 + v);
-        } else {
-          for (uint32_t i = threadIdx.x; i < cnt; i += THREADS) sv[i] = vp[i];
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < WARPS; ++e) whist[e * 256 + threadIdx.x] = 0;
-      __syncthreads();
 
-      // warp-striped items: (jj, lane) -> w*32*KPT + jj*32 + lane
-      K key[KPT];
-      V val[KPT];
-      uint32_t dig[KPT], rank[KPT];
-#pragma unroll
-      for (int jj = 0; jj < KPT; ++jj) {
-        const uint32_t idx = w * 32 * KPT + jj * 32 + lane;
-        const bool ok = idx < cnt;
-        key[jj] = sk[idx];
-        if (PAIRS) val[jj] = sv[idx];
-        dig[jj] = ok ? digit_of(key[jj], dg) : 256u;
-      }
-      warp_rank(dig, rank, mywh);
-      __syncthreads();
-
-      // per digit: exclusive offsets of each warp, tile aggregate
-      const uint32_t dd = threadIdx.x;
-      uint32_t run = 0;
-#pragma unroll
-      for (int e = 0; e < WARPS; ++e) {
-        const uint32_t x = whist[e * 256 + dd];
-        whist[e * 256 + dd] = run;
-        run += x;
-      }
-      uint32_t* my_status = status + (size_t)t * 256 + dd;
-      st_relaxed(my_status, (lt == 0 ? FLAG_INC : FLAG_AGG) | run);
-      uint32_t tot;
-      const uint32_t lstart = block_excl_scan(run, s_misc + 4, &tot);
-      uint32_t excl = 0;
-      if (lt > 0) {  // decoupled look-back over the segment's earlier tiles
-        uint32_t tt = t - 1;
-        while (true) {
-          const uint32_t v = ld_relaxed(status + (size_t)tt * 256 + dd);
-          if ((v >> 30) == 0) continue;  // predecessor not published yet
-          excl += v & VAL_MASK;
-          if (v & FLAG_INC) break;
-          --tt;
-        }
-        st_relaxed(my_status, FLAG_INC | (excl + run));
-      }
-      const uint32_t bstart = P.hist[(size_t)(s.hist_off + j) * 256 + dd];
-      s_dst[dd] = (int)(s.start + bstart + excl) - (int)lstart;
-      s_lstart[dd] = lstart;
-      __syncthreads();
-
-      // reorder the tile by digit in shared memory (stable)
-#pragma unroll
-      for (int jj = 0; jj < KPT; ++jj) {
-        if (dig[jj] < 256) {
-          const uint32_t pos = s_lstart[dig[jj]] + mywh[dig[jj]] + rank[jj];
-          sk[pos] = key[jj];
-          if (PAIRS) sv[pos] = val[jj];
-        }
-      }
-      __syncthreads();
-      // coalesced write of each digit run
-#pragma unroll 4
-      for (uint32_t i = threadIdx.x; i < cnt; i += THREADS) {
-        const K k = sk[i];
-        const int o = s_dst[digit_of(k, dg)] + (int)i;
-        dst[o] = k;
-        if (PAIRS) dstv[o] = sv[i];
-      }
-      __syncthreads();
+      if (cnt == (uint32_t)TILE)
+        deal_tile<true>(P, s, j, t, lt, cnt, dg, status, sk, sv, whist, mywh, s_dst,
+                        s_lstart, s_warp, dst, dstv);
+      else
+        deal_tile<false>(P, s, j, t, lt, cnt, dg, status, sk, sv, whist, mywh, s_dst,
+                         s_lstart, s_warp, dst, dstv);
+      fence_proxy_async();  // generic smem accesses before the next TMA into this buffer
     }
   }
 
@@ -430,7 +539,12 @@ struct Phases {
   // rank of item i inside its bucket [bs, be) of the smem composite array
   static __device__ __forceinline__ uint32_t bucket_rank(const CT* cmp, int bs, int be, CT me) {
     uint32_t r = 0;
-    for (int x = bs; x < be; ++x) r += cmp[x] < me;
+    int x = bs;
+    for (; x + 4 <= be; x += 4) {
+      const CT a = cmp[x], b = cmp[x + 1], c = cmp[x + 2], d = cmp[x + 3];
+      r += (uint32_t)(a < me) + (uint32_t)(b < me) + (uint32_t)(c < me) + (uint32_t)(d < me);
+    }
+    for (; x < be; ++x) r += cmp[x] < me;
     return r;
   }
   static __device__ __forceinline__ uint32_t bucket_rank_wide(const K* keys, int bs, int be,
@@ -479,147 +593,259 @@ struct Phases {
     }
   }
 
+  // an owned bucket > N_d starting at window position i: find its end, then
+  // queue it (Alg. 4 l.9-11)
+  static __device__ __noinline__ void divert_large(const Params<K>& P, const Seg& s, const K* sk,
+                                                   const uint32_t* bm, const K* xs, int i, int r,
+                                                   int c0, int W, int len, int shift) {
+    const int e = next_set(bm, i, W - 1);
+    uint32_t blen;
+    if (e >= 0) {
+      blen = (uint32_t)(e - i);
+    } else {
+      const K pre = (K)sk[i] >> shift;
+      uint32_t lo = (uint32_t)(c0 - 1 + (W - 1));  // last in-window index (same prefix)
+      uint32_t hi = (uint32_t)len;
+      uint32_t step = 64;
+      while (true) {  // gallop
+        const uint32_t probe = lo + step;
+        if (probe >= hi) break;
+        if ((xs[probe] >> shift) != pre) {
+          hi = probe;
+          break;
+        }
+        lo = probe;
+        step <<= 1;
+      }
+      while (hi - lo > 1) {  // first index in (lo, hi] with a different prefix
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((xs[mid] >> shift) != pre)
+          hi = mid;
+        else
+          lo = mid;
+      }
+      blen = hi - (uint32_t)r;
+    }
+    push_bucket(P, s, s.start + (uint32_t)r, blen);
+  }
+
+  // Diversion scan of one level (Alg. 4 l.7-14).  A CTA owns the buckets that
+  // START in its chunk of CH = WIN-1-N_d keys; it loads the chunk plus the key
+  // before it and a halo of N_d keys after it.  Buckets of <= N_d keys are
+  // sorted on-chip into the caller's buffer, in the stable (insertion-sort,
+  // P:194) order: a key's rank is the number of bucket keys whose composite
+  // (remaining bits, index in bucket) is smaller.  The composite is 32 bits:
+  // exact when the remaining bits R <= 24; otherwise the top 24 remaining bits
+  // and the index, and a bucket where two neighbours after ranking share
+  // those 24 bits is re-sorted exactly (insertion sort on the full keys; only
+  // keys-only u64 reaches R > 24, where equal keys are interchangeable).
+  // Larger buckets are queued (push_bucket).
+  static __device__ __forceinline__ void bucket_bounds_fast(const uint32_t* bm, int i, int& bs,
+                                                            int& be) {
+    // bits at or before i within 3 words, bits after i within 3 words (N_d <= 64)
+    const int w = i >> 5;
+    const uint32_t le = 0xffffffffu >> (31 - (i & 31));
+    const uint32_t m0 = bm[w] & le, m1 = bm[w - 1], m2 = bm[w - 2];
+    bs = m0 ? (w * 32 + 31 - __clz(m0))
+            : (m1 ? ((w - 1) * 32 + 31 - __clz(m1)) : (m2 ? ((w - 2) * 32 + 31 - __clz(m2)) : -(1 << 20)));
+    const uint32_t n0 = bm[w] & ~le, n1 = bm[w + 1], n2 = bm[w + 2];
+    be = n0 ? (w * 32 + __ffs(n0) - 1)
+            : (n1 ? ((w + 1) * 32 + __ffs(n1) - 1) : (n2 ? ((w + 2) * 32 + __ffs(n2) - 1) : (1 << 20)));
+  }
+
+  struct DivertSmem {
+    K* sk;            // window keys
+    uint32_t* cmp;    // 32-bit composites
+    uint32_t* sinfo;  // bs | be/dst << 16
+    V* sv;            // values (pairs)
+    uint32_t* bm;     // bucket-start bitmask (4 zero words on each side)
+    uint32_t* s_misc;
+  };
+
+  // one chunk of one segment; FAST: N_d <= 64 (bucket bounds within +-2 words);
+  // EXACT: the remaining bits fit the 32-bit composite (R <= 24)
+  template <bool FAST, bool EXACT>
+  static __device__ __forceinline__ void divert_chunk(const Params<K>& P, const Seg& s,
+                                                      const DivertSmem& S, int c0) {
+    K* sk = S.sk;
+    uint32_t* cmp = S.cmp;
+    uint32_t* sinfo = S.sinfo;
+    V* sv = S.sv;
+    uint32_t* bm = S.bm;
+    const int CH = (int)P.chunk;
+    const int nd = (int)P.n_d;
+    const int W = 1 + CH + nd;  // == WIN
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int len = (int)s.len;
+    const K* xs = (s.final_buf ? P.B : P.A) + s.start;
+    const V* xv = PAIRS ? (s.final_buf ? P.Bv : P.Av) + s.start : nullptr;
+    const int shift = 8 * s.low;  // remaining bits R below the group
+    const int rlo = c0 - 1;       // segment index of window position 0
+    const K remmask = (K(1) << shift) - 1;  // shift <= 56 (u64) / 24 (u32)
+    const int cshift = EXACT ? 0 : shift - 24;
+
+    // load the window
+#pragma unroll 4
+    for (int m = 0; m < KPT; ++m) {
+      const int i = threadIdx.x + THREADS * m;
+      const int r = rlo + i;
+      const bool ok = r >= 0 && r < len;
+      sk[i] = ok ? xs[r] : K(0);
+      if (PAIRS) sv[i] = ok ? xv[r] : 0u;
+    }
+    __syncthreads();
+    // bucket-start bitmask: bit i <=> a bucket (equal top-p prefix) starts at i
+#pragma unroll 4
+    for (int m = 0; m < KPT; ++m) {
+      const int i = threadIdx.x + THREADS * m;
+      const int r = rlo + i;
+      bool st = true;
+      if (r > 0 && r < len) st = (sk[i] >> shift) != (sk[i - 1] >> shift);
+      const uint32_t b = __ballot_sync(0xffffffffu, st);
+      if (lane == 0) bm[8 * m + w] = b;
+    }
+    __syncthreads();
+    // classify; composites of owned small buckets; queue owned large buckets
+#pragma unroll 2
+    for (int m = 0; m < KPT; ++m) {
+      const int i = threadIdx.x + THREADS * m;
+      const int r = rlo + i;
+      uint32_t info = 0xffffffffu;
+      int bs, be;
+      if (FAST) {
+        bucket_bounds_fast(bm, i, bs, be);
+      } else {
+        bs = prev_set(bm, i, max(1, i - nd));
+        be = bs >= 1 ? next_set(bm, i, min(W - 1, bs + nd)) : -1;
+        if (be < 0) be = 1 << 20;
+      }
+      if (i >= 1 && r < len && bs >= 1 && bs <= CH) {  // owned
+        if (be - bs <= nd) {
+          info = (uint32_t)bs | ((uint32_t)be << 16);
+          cmp[i] = ((uint32_t)((sk[i] & remmask) >> cshift) << 8) | (uint32_t)(i - bs);
+        } else if (i == bs) {
+          divert_large(P, s, sk, bm, xs, i, r, c0, W, len, shift);
+        }
+      }
+      sinfo[i] = info;
+    }
+    __syncthreads();
+    // rank inside the bucket; keys (values) and destinations into registers
+    K kreg[KPT];
+    V vreg[KPT];
+    uint32_t dreg[KPT];
+#pragma unroll
+    for (int m = 0; m < KPT; ++m) {
+      const int i = threadIdx.x + THREADS * m;
+      const uint32_t info = sinfo[i];
+      dreg[m] = info;
+      kreg[m] = sk[i];
+      if (PAIRS) vreg[m] = sv[i];
+      if (info != 0xffffffffu) {
+        const int bs = info & 0xffff, bend = info >> 16;
+        const uint32_t me = cmp[i];
+        uint32_t rk = 0;
+        int x = bs;
+#pragma unroll 1
+        for (; x + 4 <= bend; x += 4) {
+          const uint32_t a0 = cmp[x], a1 = cmp[x + 1], a2 = cmp[x + 2], a3 = cmp[x + 3];
+          rk += (uint32_t)(a0 < me) + (uint32_t)(a1 < me) + (uint32_t)(a2 < me) + (uint32_t)(a3 < me);
+        }
+#pragma unroll 1
+        for (; x < bend; ++x) rk += (uint32_t)(cmp[x] < me);
+        dreg[m] = (uint32_t)bs | ((uint32_t)(bs + rk) << 16);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < KPT; ++m) {
+      if (dreg[m] != 0xffffffffu) {
+        sk[dreg[m] >> 16] = kreg[m];
+        if (PAIRS) sv[dreg[m] >> 16] = vreg[m];
+      }
+    }
+    __syncthreads();
+    // write the sorted small buckets (coalesced); with an inexact composite,
+    // flag neighbours (same bucket) that share the top 24 remaining bits
+    K* outk = P.A + s.start;
+    V* outv = P.Av + s.start;
+    bool tie = false;
+#pragma unroll 4
+    for (int m = 0; m < KPT; ++m) {
+      if (dreg[m] != 0xffffffffu) {
+        const int i = threadIdx.x + THREADS * m;
+        const K k = sk[i];
+        outk[rlo + i] = k;
+        if (PAIRS) outv[rlo + i] = sv[i];
+        if (!EXACT && i + 1 < (int)(sinfo[i] >> 16))
+          tie |= ((k & remmask) >> cshift) == ((sk[i + 1] & remmask) >> cshift);
+      }
+    }
+    if (!EXACT) {
+      if (__syncthreads_or(tie)) {
+        // rare: re-sort each tied bucket exactly (insertion sort on full keys;
+        // R > 24 happens only for keys-only u64, where equal keys are
+        // interchangeable) and rewrite it
+#pragma unroll 1
+        for (int m = 0; m < KPT; ++m) {
+          const int i = threadIdx.x + THREADS * m;
+          const uint32_t info = sinfo[i];
+          if (info != 0xffffffffu && (int)(info & 0xffff) == i) {
+            const int e = (int)(info >> 16);
+            for (int x = i + 1; x < e; ++x) {
+              const K kx = sk[x];
+              int y = x;
+              while (y > i && sk[y - 1] > kx) {
+                sk[y] = sk[y - 1];
+                --y;
+              }
+              sk[y] = kx;
+            }
+            for (int x = i; x < e; ++x) outk[rlo + x] = sk[x];
+          }
+        }
+      }
+    }
+  }
+
   static __device__ void divert(const Params<K>& P, uint32_t* sm) {
     Ctl* c = P.ctl;
     const uint32_t total = c->total_chunks, nseg = c->nseg;
     Seg* q = P.segq[c->cur];
-    K* sk = reinterpret_cast<K*>(sm);
-    CT* cmp = reinterpret_cast<CT*>(sk + WIN);
-    V* sv = reinterpret_cast<V*>(cmp + WIN);
-    uint32_t* bm = reinterpret_cast<uint32_t*>(PAIRS ? (void*)(sv + WIN) : (void*)sv);
-    uint32_t* s_misc = bm + WIN / 32 + 8;
+    DivertSmem S;
+    S.sk = reinterpret_cast<K*>(sm);
+    S.cmp = reinterpret_cast<uint32_t*>(S.sk + WIN);
+    S.sinfo = S.cmp + WIN + 8;
+    S.sv = reinterpret_cast<V*>(S.sinfo + WIN);
+    uint32_t* bm0 = reinterpret_cast<uint32_t*>(PAIRS ? (void*)(S.sv + WIN) : (void*)S.sv);
+    S.bm = bm0 + 4;
+    S.s_misc = S.bm + WIN / 32 + 4;
     const int CH = (int)P.chunk;
-    const int nd = (int)P.n_d;
-    const int W = 1 + CH + nd;  // window: lead key, chunk, halo of N_d
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-
+    const bool fast = P.n_d <= 64;
+    if (threadIdx.x < 4) {
+      bm0[threadIdx.x] = 0;
+      S.bm[WIN / 32 + threadIdx.x] = 0;
+    }
     for (uint32_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
-      if (threadIdx.x == 0) s_misc[0] = upper_index(nseg, ch, [&](uint32_t i) { return q[i].chunk0; });
+      if (threadIdx.x == 0) S.s_misc[0] = upper_index(nseg, ch, [&](uint32_t i) { return q[i].chunk0; });
       __syncthreads();
-      const Seg s = q[s_misc[0]];
-      __syncthreads();
-      if (s.flags & (SEG_DONE | SEG_SKIP_DIVERT)) continue;
+      const Seg s = q[S.s_misc[0]];
       const int c0 = (int)(ch - s.chunk0) * CH;  // segment-relative chunk start
-      const int len = (int)s.len;
-      if (s.flags & SEG_COPY) {  // finished bucket left in B: copy out (Alg. 4 comment)
-        const int c1 = min(len, c0 + CH);
+      if (s.flags & (SEG_DONE | SEG_SKIP_DIVERT)) {
+      } else if (s.flags & SEG_COPY) {  // finished bucket left in B: copy out
+        const int c1 = min((int)s.len, c0 + CH);
         for (int r = c0 + threadIdx.x; r < c1; r += THREADS) {
           P.A[s.start + r] = P.B[s.start + r];
           if (PAIRS) P.Av[s.start + r] = P.Bv[s.start + r];
         }
-        continue;
-      }
-      const K* X = s.final_buf ? P.B : P.A;
-      const V* Xv = s.final_buf ? P.Bv : P.Av;
-      const int shift = 8 * s.low;
-      const K* xs = X + s.start;
-
-      K key[KPT];
-      V val[KPT];
-#pragma unroll
-      for (int m = 0; m < KPT; ++m) {
-        const int i = threadIdx.x + THREADS * m;
-        const int r = c0 - 1 + i;
-        const bool ok = i < W && r >= 0 && r < len;
-        key[m] = ok ? xs[r] : K(0);
-        if (PAIRS) val[m] = ok ? Xv[s.start + r] : 0u;
-        sk[i] = key[m];
-      }
-      __syncthreads();
-      // bucket-start bitmask: bit i <=> a bucket (equal top-p prefix) starts at i
-#pragma unroll
-      for (int m = 0; m < KPT; ++m) {
-        const int i = threadIdx.x + THREADS * m;
-        const int r = c0 - 1 + i;
-        bool st = false;
-        if (i < W) {
-          if (r <= 0 || r >= len)
-            st = true;
-          else
-            st = (sk[i] >> shift) != (sk[i - 1] >> shift);
-        }
-        const uint32_t b = __ballot_sync(0xffffffffu, st);
-        if (lane == 0) bm[8 * m + w] = b;
-      }
-      if (threadIdx.x < 8) bm[WIN / 32 + threadIdx.x] = 0;
-      __syncthreads();
-      // classify; composite keys of owned small buckets
-      const CT remmask = (shift >= CT_BITS) ? ~CT(0) : ((CT(1) << shift) - 1);
-      uint32_t be_[KPT];  // packed (bucket start, bucket end) or 0xffffffff
-#pragma unroll
-      for (int m = 0; m < KPT; ++m) {
-        const int i = threadIdx.x + THREADS * m;
-        const int r = c0 - 1 + i;
-        be_[m] = 0xffffffffu;
-        if (i < 1 || i >= W || r >= len) continue;
-        const int bs = prev_set(bm, i, max(1, i - nd));
-        if (bs < 1 || bs > CH) continue;  // not owned, or a bucket > N_d
-        const int bend = next_set(bm, i, min(W - 1, bs + nd));
-        if (bend >= 0) {
-          be_[m] = (uint32_t)bs | ((uint32_t)bend << 16);
-          cmp[i] = ((CT)(key[m] & (K)remmask) << 8) | (CT)(i - bs);
-        } else if (i == bs) {
-          // an owned bucket > N_d: find its end, then queue it (Alg. 4 l.9-11)
-          int e = next_set(bm, i, W - 1);
-          uint32_t blen;
-          if (e >= 0) {
-            blen = (uint32_t)(e - i);
-          } else {
-            const K pre = key[m] >> shift;
-            uint32_t lo = (uint32_t)(c0 - 1 + (W - 1));  // last in-window index (same prefix)
-            uint32_t hi = (uint32_t)len;
-            uint32_t step = 64;
-            while (true) {  // gallop
-              const uint32_t probe = lo + step;
-              if (probe >= hi) break;
-              if ((xs[probe] >> shift) != pre) {
-                hi = probe;
-                break;
-              }
-              lo = probe;
-              step <<= 1;
-            }
-            while (hi - lo > 1) {  // first index in (lo, hi] with a different prefix
-              const uint32_t mid = (lo + hi) >> 1;
-              if ((xs[mid] >> shift) != pre)
-                hi = mid;
-              else
-                lo = mid;
-            }
-            blen = hi - (uint32_t)r;
-          }
-          push_bucket(P, s, s.start + (uint32_t)r, blen);
-        }
-      }
-      __syncthreads();
-      uint32_t dst_[KPT];
-#pragma unroll
-      for (int m = 0; m < KPT; ++m) {
-        const int i = threadIdx.x + THREADS * m;
-        dst_[m] = 0;
-        if (be_[m] != 0xffffffffu) {
-          const int bs = be_[m] & 0xffff, bend = be_[m] >> 16;
-          dst_[m] = bs + bucket_rank(cmp, bs, bend, cmp[i]);
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int m = 0; m < KPT; ++m) {
-        if (be_[m] != 0xffffffffu) {
-          sk[dst_[m]] = key[m];
-          if (PAIRS) sv[dst_[m]] = val[m];
-        }
-      }
-      __syncthreads();
-      K* outk = P.A + s.start;
-      V* outv = P.Av + s.start;
-#pragma unroll
-      for (int m = 0; m < KPT; ++m) {
-        if (be_[m] != 0xffffffffu) {
-          const int i = threadIdx.x + THREADS * m;
-          const int r = c0 - 1 + i;
-          outk[r] = sk[i];
-          if (PAIRS) outv[r] = sv[i];
+      } else {
+        const bool exact = 8 * s.low <= 24;
+        if (fast) {
+          if (exact) divert_chunk<true, true>(P, s, S, c0);
+          else divert_chunk<true, false>(P, s, S, c0);
+        } else {
+          if (exact) divert_chunk<false, true>(P, s, S, c0);
+          else divert_chunk<false, false>(P, s, S, c0);
         }
       }
       __syncthreads();
@@ -629,23 +855,24 @@ struct Phases {
   // ------------------------------------------------------------------ mid
   // stable counting pass over smem range [lo, lo+L) on digit g: a -> b
   static __device__ void smem_pass(const K* a, K* b, const V* av, V* bv, int lo, int L, int g,
-                                   uint32_t* whist, uint32_t* s_lstart, uint32_t* s_warp) {
+                                   uint32_t* whist, uint32_t* wmask, uint32_t* s_lstart,
+                                   uint32_t* s_warp) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int e = 0; e < WARPS; ++e) whist[e * 256 + threadIdx.x] = 0;
     __syncthreads();
     K key[KPT];
     V val[KPT];
-    uint32_t dig[KPT], rank[KPT];
+    uint32_t dr[KPT];
 #pragma unroll
     for (int jj = 0; jj < KPT; ++jj) {
       const int rel = w * 32 * KPT + jj * 32 + lane;
       const bool ok = rel < L;
       key[jj] = ok ? a[lo + rel] : K(0);
       if (PAIRS) val[jj] = ok ? av[lo + rel] : 0u;
-      dig[jj] = ok ? digit_of(key[jj], g) : 256u;
+      dr[jj] = ok ? digit_of(key[jj], g) : 256u;
     }
-    warp_rank(dig, rank, whist + w * 256);
+    warp_rank<KPT, false>(dr, whist + w * 256);
     __syncthreads();
     uint32_t run = 0;
 #pragma unroll
@@ -659,8 +886,9 @@ struct Phases {
     __syncthreads();
 #pragma unroll
     for (int jj = 0; jj < KPT; ++jj) {
-      if (dig[jj] < 256) {
-        const int pos = lo + s_lstart[dig[jj]] + whist[w * 256 + dig[jj]] + rank[jj];
+      const uint32_t dgt = dr[jj] & 0xffffu;
+      if (dgt < 256) {
+        const int pos = lo + s_lstart[dgt] + whist[w * 256 + dgt] + (dr[jj] >> 16);
         b[pos] = key[jj];
         if (PAIRS) bv[pos] = val[jj];
       }
@@ -680,14 +908,18 @@ struct Phases {
     V* V0 = reinterpret_cast<V*>(S1 + MID_CAP);
     V* V1 = PAIRS ? V0 + MID_CAP : V0;
     CT* cmp = reinterpret_cast<CT*>(PAIRS ? (void*)(V1 + MID_CAP) : (void*)V0);
-    uint32_t* whist = reinterpret_cast<uint32_t*>(cmp + MID_CAP);
-    uint32_t* s_lstart = whist + WARPS * 256;
+    uint32_t* whist = reinterpret_cast<uint32_t*>(cmp + MID_CAP + 8);
+    uint32_t* wmask = whist + WARPS * 256;  // 2*WARPS*256, kept zero between uses
+    uint32_t* s_lstart = wmask + 2 * WARPS * 256;
     uint32_t* bm = s_lstart + 256;                   // MID_CAP/32 + 8 words
     uint2* stack = reinterpret_cast<uint2*>(bm + MID_CAP / 32 + 8);  // 512 entries
     uint32_t* s_misc = reinterpret_cast<uint32_t*>(stack + 512);     // 32 words
     unsigned long long* s_diff = reinterpret_cast<unsigned long long*>(s_misc + 16);
     const int nd = (int)P.n_d;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int e = 0; e < 2 * WARPS; ++e) wmask[e * 256 + threadIdx.x] = 0;
+    __syncthreads();
 
     for (uint32_t e = blockIdx.x; e < total; e += gridDim.x) {
       const MidE me = P.midq[e];
@@ -743,7 +975,7 @@ struct Phases {
           for (int dd = hn; dd >= 0 && ng < pmax; --dd)
             if ((diff >> (8 * dd)) & 255ull) gd[ng++] = dd;
           for (int x = ng - 1; x >= 0; --x) {  // least significant of the group first
-            smem_pass(S0, S1, V0, V1, lo, L, gd[x], whist, s_lstart, s_misc + 8);
+            smem_pass(S0, S1, V0, V1, lo, L, gd[x], whist, wmask, s_lstart, s_misc + 8);
             for (int i = threadIdx.x; i < L; i += THREADS) {
               S0[lo + i] = S1[lo + i];
               if (PAIRS) V0[lo + i] = V1[lo + i];

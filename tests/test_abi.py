@@ -14,13 +14,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "dfr.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(dfr_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|uint64_t|const char\*)\s+(dfr_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
     L = dfr.lib()
     decl = _declared()
-    assert len(decl) == 13
+    assert len(decl) == 14
     assert sorted(dfr.EXPORTS) == decl
     for name in decl:
         assert hasattr(L, name), name

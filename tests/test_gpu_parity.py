@@ -153,13 +153,13 @@ def test_stats_level0_structure():
     _, _, ost = oracle.dfr_sort(k)
     assert st["level0_p"] == ost["level0_p"] == 2
     assert st["level0_large"] == ost["level0_large"] == 0
-    assert st["reserved"] == 0  # no queue overflow
+    assert st["overflow"] == 0  # no queue overflow
     k, _ = datagen.make_case("c3-zipf", 1 << 20)
     _, _, st = gpu_sort(k, stats=True)
     _, _, ost = oracle.dfr_sort(k)
     assert st["level0_p"] == ost["level0_p"]
     assert st["level0_large"] == ost["level0_large"]
-    assert st["reserved"] == 0
+    assert st["overflow"] == 0
 
 
 def test_stream_and_repeat():
@@ -175,3 +175,19 @@ def test_stream_and_repeat():
     s.synchronize()
     assert (to_host(a, np.uint64) == to_host(b, np.uint64)).all()
     assert (to_host(a, np.uint64) == np.sort(k)).all()
+
+
+def test_divert_tie_fallback():
+    """u64 buckets whose keys share the top 24 of their remaining 40 bits and
+    differ only below: the 32-bit rank composite ties and the exact re-sort of
+    the diversion must restore the order."""
+    rng = np.random.default_rng(5)
+    n = 300000
+    prefix = rng.integers(0, 6000, n, dtype=np.uint64) << np.uint64(40)      # ~50 per bucket
+    mid = rng.integers(0, 3, n, dtype=np.uint64) << np.uint64(16)            # few top-24 values
+    low = rng.integers(0, 1 << 16, n, dtype=np.uint64)
+    k = prefix | mid | low
+    out, _, st = gpu_sort(k, stats=True)
+    ref, _, ost = oracle.dfr_sort(k)
+    assert (out == ref).all()
+    assert st["overflow"] == 0
