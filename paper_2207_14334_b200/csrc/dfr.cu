@@ -85,9 +85,9 @@ __global__ void __launch_bounds__(THREADS) k_plan2(const __grid_constant__ Param
 }
 
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(THREADS, 3) k_scatter(const __grid_constant__ Params<K> P, int j) {
+__global__ void __launch_bounds__(256, 3) k_scatter(const __grid_constant__ Params<K> P, int j) {
   extern __shared__ __align__(16) uint32_t sm[];
-  Phases<K, PAIRS>::scatter(P, j, sm);
+  Phases<K, PAIRS>::template scatter<Phases<K, PAIRS>::SC_NT>(P, j, sm);
 }
 
 template <class K, bool PAIRS>
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(THREADS) k_levels(const __grid_constant__ Para
     grid.sync();
     for (int j = 0; j < MAX_PASSES; ++j) {
       if ((uint32_t)j >= *(volatile uint32_t*)&P.ctl->max_p) break;
-      Ph::scatter(P, j, sm);
+      Ph::template scatter<THREADS>(P, j, sm);
       grid.sync();
     }
     Ph::divert(P, sm);
@@ -207,7 +207,13 @@ static cudaError_t get_dev(Dev& out) {
     setup((const void*)k_init<K, PAIRS>, 64, &d.occ_hist);
     setup((const void*)k_hist<K, PAIRS>, Ph::SMEM_HIST, &d.occ_hist);
     setup((const void*)k_plan2<K, PAIRS>, 64, &d.occ_mid);
-    setup((const void*)k_scatter<K, PAIRS>, Ph::SMEM_SCATTER, &d.occ_scatter);
+    if (err == cudaSuccess) {  // the deal runs 512-thread CTAs
+      err = cudaFuncSetAttribute((const void*)k_scatter<K, PAIRS>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_SCATTER);
+      if (err == cudaSuccess)
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &d.occ_scatter, (const void*)k_scatter<K, PAIRS>, Ph::SC_NT, Ph::SMEM_SCATTER);
+    }
     setup((const void*)k_divert<K, PAIRS>, Ph::SMEM_DIVERT, &d.occ_divert);
     setup((const void*)k_mid<K, PAIRS>, Ph::SMEM_MID, &d.occ_mid);
     setup((const void*)k_levels<K, PAIRS>, Ph::SMEM_LEVEL, &d.occ_levels);
@@ -347,7 +353,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
         continue;
       }
       pe.begin(DFR_PHASE_SCATTER0 + j);
-      k_scatter<K, PAIRS><<<g_sc, THREADS, Ph::SMEM_SCATTER, st>>>(P, j);
+      k_scatter<K, PAIRS><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER, st>>>(P, j);
       pe.end(DFR_PHASE_SCATTER0 + j);
     }
     const uint32_t chunks = (nn + P.chunk - 1) / P.chunk;
@@ -427,7 +433,7 @@ static int stage_impl(const K* in, const uint32_t* vin, K* out, uint32_t* vout, 
     k_plan2<K, PAIRS><<<1, THREADS, 64, st>>>(P);
     DFR_CHECK_LAUNCH("k_plan2(stage)");
     const int g_sc = (int)std::min<uint32_t>(tiles, (uint32_t)(dv.sms * std::max(1, dv.occ_scatter)));
-    k_scatter<K, PAIRS><<<g_sc, THREADS, Ph::SMEM_SCATTER, st>>>(P, 0);
+    k_scatter<K, PAIRS><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER, st>>>(P, 0);
     DFR_CHECK_LAUNCH("k_scatter(stage)");
   }
   cudaError_t e = cudaGetLastError();

@@ -174,10 +174,13 @@ __device__ __forceinline__ int highest_nonconst(unsigned long long diff, int hi)
   return -1;
 }
 
-// exclusive block scan of one value per thread (THREADS threads); returns the
+// exclusive block scan of one value per thread (NT threads); returns the
 // exclusive prefix, writes the block total to *total (all threads).
+// s_warp needs NT/32 words.
+template <int NT = THREADS>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp,
                                                     uint32_t* total) {
+  constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t x = v;
 #pragma unroll
@@ -188,17 +191,17 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
   if (lane == 31) s_warp[w] = x;
   __syncthreads();
   if (w == 0) {
-    uint32_t t = lane < WARPS ? s_warp[lane] : 0;
+    uint32_t t = lane < NW ? s_warp[lane] : 0;
 #pragma unroll
-    for (int o = 1; o < WARPS; o <<= 1) {
+    for (int o = 1; o < NW; o <<= 1) {
       uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
       if (lane >= o) t += y;
     }
-    if (lane < WARPS) s_warp[lane] = t;  // inclusive per warp
+    if (lane < NW) s_warp[lane] = t;  // inclusive per warp
   }
   __syncthreads();
   uint32_t wpre = w ? s_warp[w - 1] : 0;
-  *total = s_warp[WARPS - 1];
+  *total = s_warp[NW - 1];
   __syncthreads();
   return wpre + x - v;
 }

@@ -33,9 +33,9 @@ struct Phases {
 
   // ------------------------------------------------------------ smem sizes
   static constexpr size_t SMEM_HIST = WARPS * MAX_PASSES * 256 * 4 + 64;
-  static constexpr int SCATTER_HDR_WORDS = WARPS * 256 + 256 * 2 + 32;
+  static constexpr int SCATTER_HDR_WORDS = (256 / 32 + 1) * 256 + 256 + 32;
   static constexpr size_t SMEM_SCATTER =
-      SCATTER_HDR_WORDS * 4 + TILE * sizeof(K) + (PAIRS ? TILE * 4 : 0);
+      SCATTER_HDR_WORDS * 4 + 2 * TILE * sizeof(K) + (PAIRS ? 2 * TILE * 4 : 0);
   static constexpr size_t SMEM_DIVERT =
       WIN * sizeof(K) + (WIN + 8) * 4 + WIN * 4 + (PAIRS ? WIN * 4 : 0) + (WIN / 32 + 16) * 4;
   static constexpr size_t SMEM_MID = 2 * MID_CAP * sizeof(K) + (PAIRS ? 2 * MID_CAP * 4 : 0) +
@@ -343,49 +343,64 @@ struct Phases {
     return s.buf ^ (before & 1u);
   }
 
+  // The deal kernel runs SC_NT threads per CTA (16 warps) over tiles of TILE
+  // keys: SC_KPT keys per thread.  32 warps per SM hide the look-back and
+  // load latencies better than 24 and halve each warp's ranking chain.
+  static constexpr int SC_NT = 256;
+
   // rank, publish, reorder, look back, write out — one staged tile
-  template <bool FULL>
-  static __device__ __forceinline__ void deal_tile(const Params<K>& P, const Seg& s, int j,
+  template <int SC_NT, bool FULL, class Hook>
+  static __device__ __forceinline__ void deal_tile(const Hook& after_lookback, const Params<K>& P,
+                                                   const Seg& s, int j,
                                                    uint32_t t, uint32_t lt, uint32_t cnt, int dg,
                                                    uint32_t* status, K* sk, V* sv, uint32_t* whist,
-                                                   uint32_t* mywh, int* s_dst,
-                                                   uint32_t* s_lstart, uint32_t* s_warp, K* dst,
-                                                   V* dstv) {
+                                                   int* s_dst, uint32_t* s_warp, K* dst, V* dstv) {
+    constexpr int SC_W = SC_NT / 32;
+    constexpr int SC_KPT = TILE / SC_NT;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    // warp-striped items: (jj, lane) -> w*32*KPT + jj*32 + lane
-    K key[KPT];
-    V val[KPT];
-    uint32_t dr[KPT];
+    uint32_t* mywh = whist + w * 256;
+    uint32_t* tcount = whist + SC_W * 256;  // 256 tile counts (zeroed with whist)
+    // warp-striped items: (jj, lane) -> w*32*SC_KPT + jj*32 + lane
+    K key[SC_KPT];
+    V val[SC_KPT];
+    uint32_t dr[SC_KPT];
+    const uint32_t tc_s = smem_u32(tcount);
 #pragma unroll
-    for (int jj = 0; jj < KPT; ++jj) {
-      const uint32_t idx = w * 32 * KPT + jj * 32 + lane;
+    for (int jj = 0; jj < SC_KPT; ++jj) {
+      const uint32_t idx = w * 32 * SC_KPT + jj * 32 + lane;
       key[jj] = sk[idx];
       if (PAIRS) val[jj] = sv[idx];
       dr[jj] = (FULL || idx < cnt) ? digit_of(key[jj], dg) : 256u;
+      if (FULL || idx < cnt) red_add_shared(tc_s + 4 * dr[jj], 1u);  // tile histogram
     }
-    warp_rank<KPT, FULL>(dr, mywh);
     __syncthreads();
-    // per digit: exclusive offsets of each warp, tile aggregate -> publish
+    // publish the tile aggregate as early as possible: successors' look-backs
+    // then rarely wait for this tile
     const uint32_t dd = threadIdx.x;
+    const bool dig_thread = dd < 256;
     uint32_t run = 0;
-#pragma unroll
-    for (int e = 0; e < WARPS; ++e) {
-      const uint32_t x = whist[e * 256 + dd];
-      whist[e * 256 + dd] = run;
-      run += x;
+    if (dig_thread) {
+      run = tcount[dd];
+      st_relaxed(status + (size_t)t * 256 + dd, (lt == 0 ? FLAG_INC : FLAG_AGG) | run);
     }
-    uint32_t* my_status = status + (size_t)t * 256 + dd;
-    st_relaxed(my_status, (lt == 0 ? FLAG_INC : FLAG_AGG) | run);
+    warp_rank<SC_KPT, FULL>(dr, mywh);
     uint32_t tot;
-    const uint32_t lstart = block_excl_scan(run, s_warp, &tot);
+    const uint32_t lstart = block_excl_scan<SC_NT>(run, s_warp, &tot);  // syncs: ranks done
+    // per digit: warp bases in the tile = tile offset of the digit + counts of
+    // the digit in earlier warps
+    if (dig_thread) {
+      uint32_t acc = lstart;
 #pragma unroll
-    for (int e = 0; e < WARPS; ++e) whist[e * 256 + dd] += lstart;  // warp base in the tile
+      for (int e = 0; e < SC_W; ++e) {
+        const uint32_t x = whist[e * 256 + dd];
+        whist[e * 256 + dd] = acc;
+        acc += x;
+      }
+    }
     __syncthreads();
-    // reorder the tile by digit in shared memory (stable); this only needs the
-    // local offsets, so it runs before the look-back and gives the preceding
-    // tiles time to publish
+    // reorder the tile by digit in shared memory (stable)
 #pragma unroll
-    for (int jj = 0; jj < KPT; ++jj) {
+    for (int jj = 0; jj < SC_KPT; ++jj) {
       const uint32_t dgt = dr[jj] & 0xffffu;
       if (FULL || dgt < 256) {
         const uint32_t pos = mywh[dgt] + (dr[jj] >> 16);
@@ -393,37 +408,40 @@ struct Phases {
         if (PAIRS) sv[pos] = val[jj];
       }
     }
-    uint32_t excl = 0;
-    if (lt > 0) {  // decoupled look-back, up to 4 predecessors per round trip
-      int tt = (int)t - 1;
-      const int t0 = (int)s.tile0;  // publishes FLAG_INC, so the walk ends there
-      while (true) {
-        uint32_t v[4];
+    if (dig_thread) {
+      uint32_t excl = 0;
+      if (lt > 0) {  // decoupled look-back, up to 4 predecessors per round trip
+        int tt = (int)t - 1;
+        const int t0 = (int)s.tile0;  // publishes FLAG_INC, so the walk ends there
+        while (true) {
+          uint32_t v[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          v[k] = (tt - k >= t0) ? ld_relaxed(status + (size_t)(tt - k) * 256 + dd) : FLAG_INC;
-        int k = 0;
-        bool done = false;
+          for (int k = 0; k < 4; ++k)
+            v[k] = (tt - k >= t0) ? ld_relaxed(status + (size_t)(tt - k) * 256 + dd) : FLAG_INC;
+          int k = 0;
+          bool done = false;
 #pragma unroll
-        for (; k < 4; ++k) {
-          if ((v[k] >> 30) == 0) break;  // not published yet: retry from here
-          excl += v[k] & VAL_MASK;
-          if (v[k] & FLAG_INC) {
-            done = true;
-            break;
+          for (; k < 4; ++k) {
+            if ((v[k] >> 30) == 0) break;  // not published yet: retry from here
+            excl += v[k] & VAL_MASK;
+            if (v[k] & FLAG_INC) {
+              done = true;
+              break;
+            }
           }
+          if (done) break;
+          tt -= k;
         }
-        if (done) break;
-        tt -= k;
+        st_relaxed(status + (size_t)t * 256 + dd, FLAG_INC | (excl + run));
       }
-      st_relaxed(my_status, FLAG_INC | (excl + run));
+      const uint32_t bstart = P.hist[(size_t)(s.hist_off + j) * 256 + dd];
+      s_dst[dd] = (int)(s.start + bstart + excl) - (int)lstart;
     }
-    const uint32_t bstart = P.hist[(size_t)(s.hist_off + j) * 256 + dd];
-    s_dst[dd] = (int)(s.start + bstart + excl) - (int)lstart;
+    after_lookback();  // thread 0: claim the next tile, start its TMA load
     __syncthreads();
     // coalesced write of each digit run
 #pragma unroll 4
-    for (uint32_t i = threadIdx.x; i < (FULL ? (uint32_t)TILE : cnt); i += THREADS) {
+    for (uint32_t i = threadIdx.x; i < (FULL ? (uint32_t)TILE : cnt); i += SC_NT) {
       const K k = sk[i];
       const int o = s_dst[digit_of(k, dg)] + (int)i;
 #ifdef DFR_DEBUG
@@ -437,74 +455,98 @@ struct Phases {
     }
   }
 
+  // One stable deal on group digit low+j for every active segment.  A
+  // persistent CTA claims a tile of TILE keys by dynamic ticket (forward
+  // progress for the look-back), pulls it into shared memory with one TMA bulk
+  // copy, ranks it with the warp-level multi-split, publishes its per-digit
+  // aggregate, reorders the tile by digit in shared memory, resolves its
+  // exclusive per-digit prefix by decoupled look-back over the segment's
+  // earlier tiles and writes every digit run contiguously.
+  // thread 0: claim a ticket into ti[0..2] (ticket, segment, tma) and, for a
+  // full aligned tile of an active segment, start its TMA bulk load
+  static __device__ __forceinline__ void claim_tile(const Params<K>& P, int j, const Seg* q,
+                                                    uint32_t nseg, uint32_t total, uint32_t* ti,
+                                                    K* kb, V* vb, unsigned long long* bar) {
+    const uint32_t t = atomicAdd(&P.ctl->ticket[j], 1u);
+    ti[0] = t;
+    ti[2] = 0;
+    if (t >= total) return;
+    const uint32_t si = upper_index(nseg, t, [&](uint32_t i) { return q[i].tile0; });
+    ti[1] = si;
+    const Seg& s = q[si];
+    const uint32_t lt = t - s.tile0;
+    if (!pass_active(s, j) || s.len - lt * TILE < (uint32_t)TILE) return;
+    const uint32_t sb = src_buf(s, j);
+    const K* src = (sb ? P.B : P.A) + s.start + lt * TILE;
+    const V* srcv = PAIRS ? (sb ? P.Bv : P.Av) + s.start + lt * TILE : nullptr;
+    if ((reinterpret_cast<uintptr_t>(src) & 15) || (PAIRS && (reinterpret_cast<uintptr_t>(srcv) & 15)))
+      return;
+    fence_proxy_async();
+    const uint32_t bytes = TILE * sizeof(K) + (PAIRS ? TILE * 4 : 0);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(kb)),
+        "l"(src), "r"((uint32_t)(TILE * sizeof(K))), "r"(smem_u32(bar))
+        : "memory");
+    if (PAIRS)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(vb)),
+          "l"(srcv), "r"((uint32_t)(TILE * 4)), "r"(smem_u32(bar))
+          : "memory");
+    ti[2] = 1;
+  }
+
+  // Persistent CTA with two tile buffers.  The next tile's ticket is claimed,
+  // and its TMA load started, as soon as the current tile has published its
+  // inclusive prefix: the load and the ticket round trip overlap the current
+  // tile's write-out, and tickets are still claimed in (nearly) completion
+  // order, which keeps the look-back of later tiles short.
+  template <int SC_NT>
   static __device__ void scatter(const Params<K>& P, int j, uint32_t* sm) {
+    constexpr int SC_W = SC_NT / 32;
     Ctl* c = P.ctl;
     const uint32_t total = c->total_tiles, nseg = c->nseg;
     if ((uint32_t)j >= c->max_p) return;  // no segment of this level has pass j
     const Seg* q = P.segq[c->cur];
-    uint32_t* whist = sm;                                       // WARPS*256
-    int* s_dst = reinterpret_cast<int*>(whist + WARPS * 256);   // 256
-    uint32_t* s_lstart = reinterpret_cast<uint32_t*>(s_dst + 256);  // 256
-    uint32_t* s_warp = s_lstart + 256;                          // 8
-    uint32_t* s_misc = s_warp + 8;                              // 8: ticket, seg, tma
-    unsigned long long* bar = reinterpret_cast<unsigned long long*>(s_misc + 8);  // 8-aligned
-    K* const sk = reinterpret_cast<K*>(sm + SCATTER_HDR_WORDS);
-    V* const sv = reinterpret_cast<V*>(sk + TILE);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t* mywh = whist + w * 256;
+    uint32_t* whist = sm;                                         // SC_W*256
+    int* s_dst = reinterpret_cast<int*>(whist + (SC_W + 1) * 256);  // 256 (after tcount)
+    uint32_t* s_warp = reinterpret_cast<uint32_t*>(s_dst + 256);  // 16
+    uint32_t* ti = s_warp + 16;                                   // 2 x 4 words
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(ti + 8);  // 2, 8-aligned
+    K* const kb0 = reinterpret_cast<K*>(sm + SCATTER_HDR_WORDS);  // 2 x TILE keys
+    V* const vb0 = reinterpret_cast<V*>(kb0 + 2 * TILE);          // 2 x TILE values
     uint32_t* status = P.status + (size_t)j * P.status_stride;
     if (threadIdx.x == 0) {
-      mbar_init(bar, 1);
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
       fence_mbar_init();
+      claim_tile(P, j, q, nseg, total, ti, kb0, vb0, &bar[0]);
     }
-    uint32_t parity = 0;
+    uint32_t phases = 0;  // mbarrier parity per buffer
 
-    while (true) {
-      __syncthreads();  // previous tile fully written out; s_misc free
-      if (threadIdx.x == 0) {
-        const uint32_t t = atomicAdd(&c->ticket[j], 1u);
-        s_misc[0] = t;
-        s_misc[2] = 0;
-        if (t < total) {
-          const uint32_t si = upper_index(nseg, t, [&](uint32_t i) { return q[i].tile0; });
-          s_misc[1] = si;
-          const Seg& s = q[si];
-          const uint32_t lt = t - s.tile0;
-          if (pass_active(s, j) && s.len - lt * TILE >= (uint32_t)TILE) {
-            const uint32_t sb = src_buf(s, j);
-            const K* src = (sb ? P.B : P.A) + s.start + lt * TILE;
-            const V* srcv = PAIRS ? (sb ? P.Bv : P.Av) + s.start + lt * TILE : nullptr;
-            if (!(reinterpret_cast<uintptr_t>(src) & 15) &&
-                !(PAIRS && (reinterpret_cast<uintptr_t>(srcv) & 15))) {
-              fence_proxy_async();
-              const uint32_t bytes = TILE * sizeof(K) + (PAIRS ? TILE * 4 : 0);
-              asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                               smem_u32(bar)),
-                           "r"(bytes)
-                           : "memory");
-              asm volatile(
-                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
-                  "%2, [%3];" ::"r"(smem_u32(sk)),
-                  "l"(src), "r"((uint32_t)(TILE * sizeof(K))), "r"(smem_u32(bar))
-                  : "memory");
-              if (PAIRS)
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
-                    "%2, [%3];" ::"r"(smem_u32(sv)),
-                    "l"(srcv), "r"((uint32_t)(TILE * 4)), "r"(smem_u32(bar))
-                    : "memory");
-              s_misc[2] = 1;
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < WARPS; ++e) whist[e * 256 + threadIdx.x] = 0;
-      __syncthreads();
-      const uint32_t t = s_misc[0];
+    for (int it = 0;; ++it) {
+      const int cb = it & 1;
+      for (int e = threadIdx.x; e < (SC_W + 1) * 256; e += SC_NT) whist[e] = 0;
+      __syncthreads();  // ti[cb] visible; whist zeroed; the other buffer is free
+      const uint32_t t = ti[cb * 4 + 0];
       if (t >= total) break;
-      const Seg s = q[s_misc[1]];
-      if (!pass_active(s, j)) continue;
+      const Seg s = q[ti[cb * 4 + 1]];
+      const bool tma = ti[cb * 4 + 2] != 0;
+      K* sk = kb0 + cb * TILE;
+      V* sv = vb0 + cb * TILE;
+      auto hook = [&]() {
+        if (threadIdx.x == 0)
+          claim_tile(P, j, q, nseg, total, ti + (cb ^ 1) * 4, kb0 + (cb ^ 1) * TILE,
+                     vb0 + (cb ^ 1) * TILE, &bar[cb ^ 1]);
+      };
+      if (!pass_active(s, j)) {
+        hook();
+        continue;
+      }
       const uint32_t lt = t - s.tile0;
       const uint32_t base = s.start + lt * TILE;
       const uint32_t cnt = min((uint32_t)TILE, s.len - lt * TILE);
@@ -514,25 +556,24 @@ struct Phases {
       const V* srcv = sb ? P.Bv : P.Av;
       V* dstv = sb ? P.Av : P.Bv;
       const int dg = s.low + j;
-
-      if (s_misc[2]) {
-        mbar_wait(bar, parity);
-        parity ^= 1u;
+      if (tma) {
+        mbar_wait(&bar[cb], (phases >> cb) & 1u);
+        phases ^= 1u << cb;
       } else {  // ragged tail / unaligned tile: plain coalesced loads
-        for (uint32_t i = threadIdx.x; i < cnt; i += THREADS) sk[i] = src[base + i];
+        for (uint32_t i = threadIdx.x; i < cnt; i += SC_NT) sk[i] = src[base + i];
         if (PAIRS)
-          for (uint32_t i = threadIdx.x; i < cnt; i += THREADS) sv[i] = srcv[base + i];
+          for (uint32_t i = threadIdx.x; i < cnt; i += SC_NT) sv[i] = srcv[base + i];
         __syncthreads();
       }
-
       if (cnt == (uint32_t)TILE)
-        deal_tile<true>(P, s, j, t, lt, cnt, dg, status, sk, sv, whist, mywh, s_dst,
-                        s_lstart, s_warp, dst, dstv);
+        deal_tile<SC_NT, true>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist, s_dst, s_warp,
+                               dst, dstv);
       else
-        deal_tile<false>(P, s, j, t, lt, cnt, dg, status, sk, sv, whist, mywh, s_dst,
-                         s_lstart, s_warp, dst, dstv);
-      fence_proxy_async();  // generic smem accesses before the next TMA into this buffer
+        deal_tile<SC_NT, false>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist, s_dst,
+                                s_warp, dst, dstv);
+      fence_proxy_async();  // generic smem accesses before a later TMA into this buffer
     }
+    // every claimed ticket < total was processed, so no bulk copy is in flight here
   }
 
   // ------------------------------------------------------- small sort core
