@@ -37,7 +37,7 @@ struct Phases {
   static constexpr size_t SMEM_SCATTER =
       SCATTER_HDR_WORDS * 4 + 2 * TILE * sizeof(K) + (PAIRS ? 2 * TILE * 4 : 0);
   static constexpr size_t SMEM_DIVERT =
-      WIN * sizeof(K) + (WIN + 8) * 4 + WIN * 4 + (PAIRS ? WIN * 4 : 0) + (WIN / 32 + 16) * 4;
+      WIN * sizeof(K) + (WIN + 8) * sizeof(CT) + (PAIRS ? WIN * 4 : 0) + (WIN / 32 + 16) * 4 + 32;
   static constexpr size_t SMEM_MID = 2 * MID_CAP * sizeof(K) + (PAIRS ? 2 * MID_CAP * 4 : 0) +
                                      (MID_CAP + 8) * sizeof(CT) + 3 * WARPS * 256 * 4 + 256 * 4 +
                                      (MID_CAP / 32 + 8) * 4 + 512 * 8 + 128;
@@ -435,7 +435,8 @@ struct Phases {
         st_relaxed(status + (size_t)t * 256 + dd, FLAG_INC | (excl + run));
       }
       const uint32_t bstart = P.hist[(size_t)(s.hist_off + j) * 256 + dd];
-      s_dst[dd] = (int)(s.start + bstart + excl) - (int)lstart;
+      // run offset of the digit relative to the tile's local offsets, mod 2^32
+      s_dst[dd] = (int)(s.start + bstart + excl - lstart);
     }
     after_lookback();  // thread 0: claim the next tile, start its TMA load
     __syncthreads();
@@ -443,10 +444,10 @@ struct Phases {
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < (FULL ? (uint32_t)TILE : cnt); i += SC_NT) {
       const K k = sk[i];
-      const int o = s_dst[digit_of(k, dg)] + (int)i;
+      const uint32_t o = (uint32_t)s_dst[digit_of(k, dg)] + i;  // < 2^30: unsigned math
 #ifdef DFR_DEBUG
-      if (o < (int)s.start || o >= (int)(s.start + s.len)) {
-        printf("scatter OOB: t=%u i=%u o=%d seg=[%u,%u)\n", t, i, o, s.start, s.start + s.len);
+      if (o < s.start || o >= s.start + s.len) {
+        printf("scatter OOB: t=%u i=%u o=%u seg=[%u,%u)\n", t, i, o, s.start, s.start + s.len);
         __trap();
       }
 #endif
@@ -696,21 +697,20 @@ struct Phases {
 
   struct DivertSmem {
     K* sk;            // window keys
-    uint32_t* cmp;    // 32-bit composites
-    uint32_t* sinfo;  // bs | be/dst << 16
+    CT* cmp;          // exact composites (remaining bits << 8 | index in bucket)
     V* sv;            // values (pairs)
     uint32_t* bm;     // bucket-start bitmask (4 zero words on each side)
     uint32_t* s_misc;
+    unsigned long long* bar;
   };
 
-  // one chunk of one segment; FAST: N_d <= 64 (bucket bounds within +-2 words);
-  // EXACT: the remaining bits fit the 32-bit composite (R <= 24)
-  template <bool FAST, bool EXACT>
+  // one chunk of one segment; FAST: N_d <= 64 (bucket bounds within +-2 words)
+  template <bool FAST>
   static __device__ __forceinline__ void divert_chunk(const Params<K>& P, const Seg& s,
-                                                      const DivertSmem& S, int c0) {
+                                                      const DivertSmem& S, int c0,
+                                                      uint32_t& parity) {
     K* sk = S.sk;
-    uint32_t* cmp = S.cmp;
-    uint32_t* sinfo = S.sinfo;
+    CT* cmp = S.cmp;
     V* sv = S.sv;
     uint32_t* bm = S.bm;
     const int CH = (int)P.chunk;
@@ -720,21 +720,46 @@ struct Phases {
     const int len = (int)s.len;
     const K* xs = (s.final_buf ? P.B : P.A) + s.start;
     const V* xv = PAIRS ? (s.final_buf ? P.Bv : P.Av) + s.start : nullptr;
-    const int shift = 8 * s.low;  // remaining bits R below the group
+    const int shift = 8 * s.low;  // remaining bits R below the group (<= 56)
     const int rlo = c0 - 1;       // segment index of window position 0
-    const K remmask = (K(1) << shift) - 1;  // shift <= 56 (u64) / 24 (u32)
-    const int cshift = EXACT ? 0 : shift - 24;
+    const K remmask = (K(1) << shift) - 1;
 
-    // load the window
+    // load the window: one TMA bulk copy for an interior, 16-byte aligned window
+    const bool interior = rlo >= 0 && rlo + W <= len;
+    const bool tma = interior && !(reinterpret_cast<uintptr_t>(xs + rlo) & 15) &&
+                     !(PAIRS && (reinterpret_cast<uintptr_t>(xv + rlo) & 15));
+    if (tma) {
+      if (threadIdx.x == 0) {
+        fence_proxy_async();
+        const uint32_t bytes = WIN * sizeof(K) + (PAIRS ? WIN * 4 : 0);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(S.bar)),
+                     "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(sk)),
+            "l"(xs + rlo), "r"((uint32_t)(WIN * sizeof(K))), "r"(smem_u32(S.bar))
+            : "memory");
+        if (PAIRS)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(sv)),
+              "l"(xv + rlo), "r"((uint32_t)(WIN * 4)), "r"(smem_u32(S.bar))
+              : "memory");
+      }
+      mbar_wait(S.bar, parity);
+      parity ^= 1u;
+    } else {
 #pragma unroll 4
-    for (int m = 0; m < KPT; ++m) {
-      const int i = threadIdx.x + THREADS * m;
-      const int r = rlo + i;
-      const bool ok = r >= 0 && r < len;
-      sk[i] = ok ? xs[r] : K(0);
-      if (PAIRS) sv[i] = ok ? xv[r] : 0u;
+      for (int m = 0; m < KPT; ++m) {
+        const int i = threadIdx.x + THREADS * m;
+        const int r = rlo + i;
+        const bool ok = r >= 0 && r < len;
+        sk[i] = ok ? xs[r] : K(0);
+        if (PAIRS) sv[i] = ok ? xv[r] : 0u;
+      }
+      __syncthreads();
     }
-    __syncthreads();
     // bucket-start bitmask: bit i <=> a bucket (equal top-p prefix) starts at i
 #pragma unroll 4
     for (int m = 0; m < KPT; ++m) {
@@ -746,12 +771,13 @@ struct Phases {
       if (lane == 0) bm[8 * m + w] = b;
     }
     __syncthreads();
-    // classify; composites of owned small buckets; queue owned large buckets
-#pragma unroll 2
+    // classify; composites of owned small buckets; queue owned large buckets.
+    // The bucket bounds of each of this thread's positions stay in registers.
+    uint32_t info[KPT];
+#pragma unroll
     for (int m = 0; m < KPT; ++m) {
       const int i = threadIdx.x + THREADS * m;
       const int r = rlo + i;
-      uint32_t info = 0xffffffffu;
       int bs, be;
       if (FAST) {
         bucket_bounds_fast(bm, i, bs, be);
@@ -760,91 +786,39 @@ struct Phases {
         be = bs >= 1 ? next_set(bm, i, min(W - 1, bs + nd)) : -1;
         if (be < 0) be = 1 << 20;
       }
+      info[m] = 0xffffffffu;
       if (i >= 1 && r < len && bs >= 1 && bs <= CH) {  // owned
         if (be - bs <= nd) {
-          info = (uint32_t)bs | ((uint32_t)be << 16);
-          cmp[i] = ((uint32_t)((sk[i] & remmask) >> cshift) << 8) | (uint32_t)(i - bs);
+          info[m] = (uint32_t)bs | ((uint32_t)be << 16);
+          cmp[i] = ((CT)(sk[i] & remmask) << 8) | (CT)(i - bs);
         } else if (i == bs) {
           divert_large(P, s, sk, bm, xs, i, r, c0, W, len, shift);
         }
       }
-      sinfo[i] = info;
     }
     __syncthreads();
-    // rank inside the bucket; keys (values) and destinations into registers
-    K kreg[KPT];
-    V vreg[KPT];
-    uint32_t dreg[KPT];
+    // rank inside the bucket; write each key straight to its slot in the
+    // caller's buffer (a permutation inside a ~16-key bucket: the warp's
+    // stores stay within a few 128-byte segments)
+    K* outk = P.A + s.start + rlo;
+    V* outv = P.Av + s.start + rlo;
 #pragma unroll
     for (int m = 0; m < KPT; ++m) {
-      const int i = threadIdx.x + THREADS * m;
-      const uint32_t info = sinfo[i];
-      dreg[m] = info;
-      kreg[m] = sk[i];
-      if (PAIRS) vreg[m] = sv[i];
-      if (info != 0xffffffffu) {
-        const int bs = info & 0xffff, bend = info >> 16;
-        const uint32_t me = cmp[i];
+      if (info[m] != 0xffffffffu) {
+        const int i = threadIdx.x + THREADS * m;
+        const int bs = info[m] & 0xffff, bend = info[m] >> 16;
+        const CT me = cmp[i];
+        // count over [bs, bs + 4*ceil(len/4)), then take back the overrun
+        const int stop = bs + ((bend - bs + 3) & ~3);
         uint32_t rk = 0;
-        int x = bs;
 #pragma unroll 1
-        for (; x + 4 <= bend; x += 4) {
-          const uint32_t a0 = cmp[x], a1 = cmp[x + 1], a2 = cmp[x + 2], a3 = cmp[x + 3];
+        for (int x = bs; x < stop; x += 4) {
+          const CT a0 = cmp[x], a1 = cmp[x + 1], a2 = cmp[x + 2], a3 = cmp[x + 3];
           rk += (uint32_t)(a0 < me) + (uint32_t)(a1 < me) + (uint32_t)(a2 < me) + (uint32_t)(a3 < me);
         }
-#pragma unroll 1
-        for (; x < bend; ++x) rk += (uint32_t)(cmp[x] < me);
-        dreg[m] = (uint32_t)bs | ((uint32_t)(bs + rk) << 16);
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int m = 0; m < KPT; ++m) {
-      if (dreg[m] != 0xffffffffu) {
-        sk[dreg[m] >> 16] = kreg[m];
-        if (PAIRS) sv[dreg[m] >> 16] = vreg[m];
-      }
-    }
-    __syncthreads();
-    // write the sorted small buckets (coalesced); with an inexact composite,
-    // flag neighbours (same bucket) that share the top 24 remaining bits
-    K* outk = P.A + s.start;
-    V* outv = P.Av + s.start;
-    bool tie = false;
-#pragma unroll 4
-    for (int m = 0; m < KPT; ++m) {
-      if (dreg[m] != 0xffffffffu) {
-        const int i = threadIdx.x + THREADS * m;
-        const K k = sk[i];
-        outk[rlo + i] = k;
-        if (PAIRS) outv[rlo + i] = sv[i];
-        if (!EXACT && i + 1 < (int)(sinfo[i] >> 16))
-          tie |= ((k & remmask) >> cshift) == ((sk[i + 1] & remmask) >> cshift);
-      }
-    }
-    if (!EXACT) {
-      if (__syncthreads_or(tie)) {
-        // rare: re-sort each tied bucket exactly (insertion sort on full keys;
-        // R > 24 happens only for keys-only u64, where equal keys are
-        // interchangeable) and rewrite it
-#pragma unroll 1
-        for (int m = 0; m < KPT; ++m) {
-          const int i = threadIdx.x + THREADS * m;
-          const uint32_t info = sinfo[i];
-          if (info != 0xffffffffu && (int)(info & 0xffff) == i) {
-            const int e = (int)(info >> 16);
-            for (int x = i + 1; x < e; ++x) {
-              const K kx = sk[x];
-              int y = x;
-              while (y > i && sk[y - 1] > kx) {
-                sk[y] = sk[y - 1];
-                --y;
-              }
-              sk[y] = kx;
-            }
-            for (int x = i; x < e; ++x) outk[rlo + x] = sk[x];
-          }
-        }
+        for (int x = bend; x < stop; ++x) rk -= (uint32_t)(cmp[x] < me);
+        outk[bs + rk] = sk[i];
+        if (PAIRS) outv[bs + rk] = sv[i];
       }
     }
   }
@@ -855,18 +829,24 @@ struct Phases {
     Seg* q = P.segq[c->cur];
     DivertSmem S;
     S.sk = reinterpret_cast<K*>(sm);
-    S.cmp = reinterpret_cast<uint32_t*>(S.sk + WIN);
-    S.sinfo = S.cmp + WIN + 8;
-    S.sv = reinterpret_cast<V*>(S.sinfo + WIN);
+    S.cmp = reinterpret_cast<CT*>(S.sk + WIN);
+    S.sv = reinterpret_cast<V*>(S.cmp + WIN + 8);
     uint32_t* bm0 = reinterpret_cast<uint32_t*>(PAIRS ? (void*)(S.sv + WIN) : (void*)S.sv);
     S.bm = bm0 + 4;
     S.s_misc = S.bm + WIN / 32 + 4;
+    S.bar = reinterpret_cast<unsigned long long*>(S.s_misc + 8);
     const int CH = (int)P.chunk;
     const bool fast = P.n_d <= 64;
     if (threadIdx.x < 4) {
       bm0[threadIdx.x] = 0;
       S.bm[WIN / 32 + threadIdx.x] = 0;
     }
+    if (threadIdx.x < 8) S.cmp[WIN + threadIdx.x] = ~CT(0);  // overrun pad (taken back)
+    if (threadIdx.x == 0) {
+      mbar_init(S.bar, 1);
+      fence_mbar_init();
+    }
+    uint32_t parity = 0;
     for (uint32_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
       if (threadIdx.x == 0) S.s_misc[0] = upper_index(nseg, ch, [&](uint32_t i) { return q[i].chunk0; });
       __syncthreads();
@@ -880,16 +860,13 @@ struct Phases {
           if (PAIRS) P.Av[s.start + r] = P.Bv[s.start + r];
         }
       } else {
-        const bool exact = 8 * s.low <= 24;
-        if (fast) {
-          if (exact) divert_chunk<true, true>(P, s, S, c0);
-          else divert_chunk<true, false>(P, s, S, c0);
-        } else {
-          if (exact) divert_chunk<false, true>(P, s, S, c0);
-          else divert_chunk<false, false>(P, s, S, c0);
-        }
+        if (fast)
+          divert_chunk<true>(P, s, S, c0, parity);
+        else
+          divert_chunk<false>(P, s, S, c0, parity);
       }
       __syncthreads();
+      fence_proxy_async();  // generic smem accesses before the next TMA into the window
     }
   }
 
