@@ -91,9 +91,9 @@ __global__ void __launch_bounds__(256, 3) k_scatter(const __grid_constant__ Para
 }
 
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(THREADS, 3) k_divert(const __grid_constant__ Params<K> P) {
+__global__ void __launch_bounds__(Phases<K, PAIRS>::DV_NT, 4) k_divert(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
-  Phases<K, PAIRS>::divert(P, sm);
+  Phases<K, PAIRS>::template divert<Phases<K, PAIRS>::DV_NT>(P, sm);
 }
 
 template <class K, bool PAIRS>
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(THREADS) k_levels(const __grid_constant__ Para
       Ph::template scatter<THREADS>(P, j, sm);
       grid.sync();
     }
-    Ph::divert(P, sm);
+    Ph::template divert<THREADS>(P, sm);
     grid.sync();
   }
 }
@@ -214,7 +214,13 @@ static cudaError_t get_dev(Dev& out) {
         err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &d.occ_scatter, (const void*)k_scatter<K, PAIRS>, Ph::SC_NT, Ph::SMEM_SCATTER);
     }
-    setup((const void*)k_divert<K, PAIRS>, Ph::SMEM_DIVERT, &d.occ_divert);
+    if (err == cudaSuccess) {  // the diversion runs DV_NT-thread CTAs
+      err = cudaFuncSetAttribute((const void*)k_divert<K, PAIRS>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_DIVERT);
+      if (err == cudaSuccess)
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &d.occ_divert, (const void*)k_divert<K, PAIRS>, Ph::DV_NT, Ph::SMEM_DIVERT);
+    }
     setup((const void*)k_mid<K, PAIRS>, Ph::SMEM_MID, &d.occ_mid);
     setup((const void*)k_levels<K, PAIRS>, Ph::SMEM_LEVEL, &d.occ_levels);
     devs[dev] = d;
@@ -261,8 +267,9 @@ static Layout make_layout(size_t n, int kb, int vb, uint32_t n_d, int min_passes
 
 template <class K>
 static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals, bool pairs,
-                             uint32_t n_d, uint32_t skip) {
+                             uint32_t n_d, uint32_t skip, size_t n) {
   Params<K> P{};
+  P.n = (uint32_t)n;
   P.A = keys;
   P.B = reinterpret_cast<K*>(ws + L.b_keys);
   P.Av = vals;
@@ -278,7 +285,7 @@ static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals,
   P.mid_cap = (uint32_t)L.mid_cap;
   P.hist_rows = (uint32_t)L.hist_rows;
   P.n_d = n_d;
-  P.chunk = WIN - 1 - n_d;
+  P.chunk = WIN - (uint32_t)(16 / sizeof(K)) - n_d;
   P.skip_trivial = skip;
   P.D = (int)sizeof(K);
   return P;
@@ -322,7 +329,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
     cudaGetLastError();
     return DFR_ERR_ALLOC;
   }
-  Params<K> P = make_params<K>(ws, L, keys, vals, PAIRS, n_d, skip);
+  Params<K> P = make_params<K>(ws, L, keys, vals, PAIRS, n_d, skip, n);
   const uint32_t nn = (uint32_t)n;
   const int sms = dv.sms;
   const PhaseEv pe{cfg ? cfg->phase_events : nullptr, st};
@@ -359,7 +366,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
     const uint32_t chunks = (nn + P.chunk - 1) / P.chunk;
     const int g_dv = (int)std::min<uint32_t>(chunks, (uint32_t)(sms * std::max(1, dv.occ_divert)));
     pe.begin(DFR_PHASE_DIVERT);
-    k_divert<K, PAIRS><<<g_dv, THREADS, Ph::SMEM_DIVERT, st>>>(P);
+    k_divert<K, PAIRS><<<g_dv, Ph::DV_NT, Ph::SMEM_DIVERT, st>>>(P);
     pe.end(DFR_PHASE_DIVERT);
     pe.begin(DFR_PHASE_LEVELS);
     void* args[] = {&P};
@@ -416,7 +423,7 @@ static int stage_impl(const K* in, const uint32_t* vin, K* out, uint32_t* vout, 
     cudaGetLastError();
     return DFR_ERR_ALLOC;
   }
-  Params<K> P = make_params<K>(ws, L, const_cast<K*>(in), const_cast<uint32_t*>(vin), PAIRS, 64, 0);
+  Params<K> P = make_params<K>(ws, L, const_cast<K*>(in), const_cast<uint32_t*>(vin), PAIRS, 64, 0, n);
   P.B = out;  // pass 0 deals A=in -> B=out
   P.Bv = vout;
   const uint32_t nn = (uint32_t)n;

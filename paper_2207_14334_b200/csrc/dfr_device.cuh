@@ -11,6 +11,7 @@
 #pragma once
 #include <cooperative_groups.h>
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace dfr {
@@ -19,7 +20,7 @@ constexpr int THREADS = 256;             // one CTA = 8 warps
 constexpr int WARPS = THREADS / 32;
 constexpr int KPT = 16;                  // keys per thread per tile
 constexpr int TILE = THREADS * KPT;      // 4096 keys per tile (hist / deal)
-constexpr int WIN = TILE;                // diversion window (keys) per CTA
+constexpr int WIN = 2048;                // diversion window (keys) per CTA
 constexpr int MID_CAP = 4096;            // C: buckets N_d < s <= C finish on-chip
 constexpr int MAX_ND = 256;              // composite index uses 8 bits
 constexpr int MAX_PASSES = 4;            // top passes per group (p <= 3 for n < 2^30)
@@ -89,7 +90,8 @@ struct Params {
   uint32_t mid_cap;     // capacity of midq
   uint32_t hist_rows;   // capacity of hist (rows)
   uint32_t n_d;         // diversion threshold N_d
-  uint32_t chunk;       // diversion chunk = WIN - 1 - n_d
+  uint32_t chunk;       // diversion chunk = WIN - 16/sizeof(K) - n_d
+  uint32_t n;           // elements of the whole array
   uint32_t skip_trivial;
   int D;                // digits per key
 };
@@ -150,6 +152,45 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// explicit shared-space accesses on 32-bit shared addresses (the compiler
+// otherwise falls back to generic LD/ST when smem pointers travel in structs)
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64v(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T ldsk(uint32_t a);
+template <>
+__device__ __forceinline__ uint32_t ldsk<uint32_t>(uint32_t a) { return lds32(a); }
+template <>
+__device__ __forceinline__ unsigned long long ldsk<unsigned long long>(uint32_t a) {
+  unsigned long long v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
 }
 
 __device__ __forceinline__ void red_add_shared(uint32_t saddr, uint32_t v) {

@@ -36,8 +36,9 @@ struct Phases {
   static constexpr int SCATTER_HDR_WORDS = (256 / 32 + 1) * 256 + 256 + 32;
   static constexpr size_t SMEM_SCATTER =
       SCATTER_HDR_WORDS * 4 + 2 * TILE * sizeof(K) + (PAIRS ? 2 * TILE * 4 : 0);
-  static constexpr size_t SMEM_DIVERT =
-      WIN * sizeof(K) + (WIN + 8) * sizeof(CT) + (PAIRS ? WIN * 4 : 0) + (WIN / 32 + 16) * 4 + 32;
+  // 2 windows (+ values) | fp16 composites | order | bitmask, misc, mbarriers
+  static constexpr size_t SMEM_DIVERT = 2 * (WIN * sizeof(K) + (PAIRS ? WIN * 4 : 0)) +
+                                        (4 * WIN + 64) * 2 + WIN * 2 + (WIN / 32 + 12) * 4 + 16 + 16;
   static constexpr size_t SMEM_MID = 2 * MID_CAP * sizeof(K) + (PAIRS ? 2 * MID_CAP * 4 : 0) +
                                      (MID_CAP + 8) * sizeof(CT) + 3 * WARPS * 256 * 4 + 256 * 4 +
                                      (MID_CAP / 32 + 8) * 4 + 512 * 8 + 128;
@@ -635,53 +636,6 @@ struct Phases {
     }
   }
 
-  // an owned bucket > N_d starting at window position i: find its end, then
-  // queue it (Alg. 4 l.9-11)
-  static __device__ __noinline__ void divert_large(const Params<K>& P, const Seg& s, const K* sk,
-                                                   const uint32_t* bm, const K* xs, int i, int r,
-                                                   int c0, int W, int len, int shift) {
-    const int e = next_set(bm, i, W - 1);
-    uint32_t blen;
-    if (e >= 0) {
-      blen = (uint32_t)(e - i);
-    } else {
-      const K pre = (K)sk[i] >> shift;
-      uint32_t lo = (uint32_t)(c0 - 1 + (W - 1));  // last in-window index (same prefix)
-      uint32_t hi = (uint32_t)len;
-      uint32_t step = 64;
-      while (true) {  // gallop
-        const uint32_t probe = lo + step;
-        if (probe >= hi) break;
-        if ((xs[probe] >> shift) != pre) {
-          hi = probe;
-          break;
-        }
-        lo = probe;
-        step <<= 1;
-      }
-      while (hi - lo > 1) {  // first index in (lo, hi] with a different prefix
-        const uint32_t mid = (lo + hi) >> 1;
-        if ((xs[mid] >> shift) != pre)
-          hi = mid;
-        else
-          lo = mid;
-      }
-      blen = hi - (uint32_t)r;
-    }
-    push_bucket(P, s, s.start + (uint32_t)r, blen);
-  }
-
-  // Diversion scan of one level (Alg. 4 l.7-14).  A CTA owns the buckets that
-  // START in its chunk of CH = WIN-1-N_d keys; it loads the chunk plus the key
-  // before it and a halo of N_d keys after it.  Buckets of <= N_d keys are
-  // sorted on-chip into the caller's buffer, in the stable (insertion-sort,
-  // P:194) order: a key's rank is the number of bucket keys whose composite
-  // (remaining bits, index in bucket) is smaller.  The composite is 32 bits:
-  // exact when the remaining bits R <= 24; otherwise the top 24 remaining bits
-  // and the index, and a bucket where two neighbours after ranking share
-  // those 24 bits is re-sorted exactly (insertion sort on the full keys; only
-  // keys-only u64 reaches R > 24, where equal keys are interchangeable).
-  // Larger buckets are queued (push_bucket).
   static __device__ __forceinline__ void bucket_bounds_fast(const uint32_t* bm, int i, int& bs,
                                                             int& be) {
     // bits at or before i within 3 words, bits after i within 3 words (N_d <= 64)
@@ -695,178 +649,438 @@ struct Phases {
             : (n1 ? ((w + 1) * 32 + __ffs(n1) - 1) : (n2 ? ((w + 2) * 32 + __ffs(n2) - 1) : (1 << 20)));
   }
 
+  // Diversion scan of one level (Alg. 4 l.7-14).  A CTA owns the buckets that
+  // START in its chunk of CH = WIN - VEC - N_d keys; it holds one window of
+  // WIN keys (16-byte aligned start <= chunk start - 1; TMA bulk copies,
+  // double-buffered one window ahead) so that every owned bucket of <= N_d
+  // keys lies inside the window.  Those are sorted on-chip into the caller's
+  // buffer in the stable (insertion-sort) order; larger buckets are
+  // queued (Alg. 4 l.11).
+  //
+  // Per window (DV_NT threads, DKPT positions each, position i = tid + DV_NT*m):
+  //   A  keys -> registers; bucket-start bitmask by ballot; composites := +inf
+  //   B  bucket bounds from the bitmask; the 16-bit composite of each owned
+  //      small-bucket key at cmp[4*bs + idx] (4-aligned groups per bucket)
+  //   C  rank = number of bucket keys with a smaller composite, counted four
+  //      at a time with packed fp16x2 compares (HSET2 + HADD2; composites are
+  //      positive normal fp16 bit patterns, so integer order = fp16 order);
+  //      order[bs + rank] = i
+  //   D  (lossy composites) read-back: a slot claimed by another key means a
+  //      tie -> that bucket is re-ranked exactly on the full keys by a warp
+  //   E  coalesced write of every owned slot: out[j] = window[order[j]]
+  // The composite is exact — (remaining bits, index in bucket) — when the R
+  // remaining bits fit 14 - idx bits; otherwise it is the top 14 remaining bits.
+  static constexpr uint16_t H_INF = 0x7c00;   // +inf: never below a composite
+  static constexpr uint16_t H_BASE = 0x0400;  // smallest positive normal fp16
+  static constexpr uint32_t DV_NONE = 0xffffffffu;
+  static constexpr int DV_NT = 256;           // threads of the stand-alone divert kernel
+  static constexpr size_t DV_WIN_BYTES = WIN * sizeof(K) + (PAIRS ? WIN * 4 : 0);
+  static constexpr int DV_CMP = 4 * WIN + 64;  // halves
+
   struct DivertSmem {
-    K* sk;            // window keys
-    CT* cmp;          // exact composites (remaining bits << 8 | index in bucket)
-    V* sv;            // values (pairs)
-    uint32_t* bm;     // bucket-start bitmask (4 zero words on each side)
-    uint32_t* s_misc;
-    unsigned long long* bar;
+    char* win[2];       // double-buffered windows: keys, then values (pairs)
+    uint16_t* cmp;      // fp16 composites
+    uint16_t* order;    // slot -> window position of the key ranked there
+    uint32_t* bm;       // bucket-start bitmask (4 zero words on each side)
+    uint32_t* misc;     // [2*b]: segment of the window in buffer b, [2*b+1]: tma flag
+    unsigned long long* bar;  // one mbarrier per buffer
   };
 
-  // one chunk of one segment; FAST: N_d <= 64 (bucket bounds within +-2 words)
-  template <bool FAST>
-  static __device__ __forceinline__ void divert_chunk(const Params<K>& P, const Seg& s,
-                                                      const DivertSmem& S, int c0,
-                                                      uint32_t& parity) {
-    K* sk = S.sk;
-    CT* cmp = S.cmp;
-    V* sv = S.sv;
-    uint32_t* bm = S.bm;
+  // composite of a key with R remaining bits at index idx of its bucket
+  struct Compo {
+    K mask;        // remaining bits
+    int sh, sl;    // (rem >> sh) << sl
+    uint32_t im;   // index mask (exact mode)
+    bool exact;
+    __device__ __forceinline__ void init(int R, int nd) {
+      const int idxb = nd <= 64 ? 6 : 8;
+      mask = R ? (K)(~K(0) >> (8 * sizeof(K) - R)) : K(0);
+      exact = R + idxb <= 14;
+      sh = exact ? 0 : R - 14;
+      sl = exact ? idxb : 0;
+      im = exact ? 0xffu : 0u;
+    }
+    __device__ __forceinline__ uint16_t operator()(K k, uint32_t idx) const {
+      return (uint16_t)(H_BASE + (((uint32_t)((k & mask) >> sh) << sl) | (idx & im)));
+    }
+    // LOSSY: top 14 of the R remaining bits; exact: (rem << idxb) | idx
+    template <bool LOSSY>
+    __device__ __forceinline__ uint16_t get(K k, uint32_t idx) const {
+      if (LOSSY) return (uint16_t)(H_BASE + ((uint32_t)(k >> sh) & 0x3fffu));
+      return (uint16_t)(H_BASE + (((uint32_t)(k & mask) << sl) | idx));
+    }
+  };
+
+  // window geometry of chunk ch of segment s: r0 = segment index of window
+  // position 0 (16-byte aligned in memory), off = first owned position
+  static __device__ __forceinline__ void window_of(const Params<K>& P, const Seg& s, uint32_t ch,
+                                                   int& c0, int& r0, int& off) {
+    constexpr int VEC = 16 / sizeof(K);
+    c0 = (int)(ch - s.chunk0) * (int)P.chunk;
+    const long long a = (long long)s.start + c0 - 1;  // absolute index of the key before the chunk
+    const long long a0 = a >= 0 ? (a & ~(long long)(VEC - 1)) : -(long long)VEC;
+    r0 = (int)(a0 - (long long)s.start);
+    off = c0 - r0;
+  }
+
+  // thread 0: chunk ch goes to buffer b; start its TMA when the window lies
+  // inside the array and the segment diverts this level
+  static __device__ __forceinline__ void divert_prefetch(const Params<K>& P, const Seg* q,
+                                                         uint32_t nseg, uint32_t total,
+                                                         uint32_t ch, const DivertSmem& S, int b) {
+    S.misc[2 * b] = 0;
+    S.misc[2 * b + 1] = 0;
+    if (ch >= total) return;
+    const uint32_t si = upper_index(nseg, ch, [&](uint32_t i) { return q[i].chunk0; });
+    S.misc[2 * b] = si;
+    const Seg& s = q[si];
+    if (s.flags & (SEG_DONE | SEG_SKIP_DIVERT | SEG_COPY)) return;
+    int c0, r0, off;
+    window_of(P, s, ch, c0, r0, off);
+    const long long abs0 = (long long)s.start + r0;
+    if (abs0 < 0 || abs0 + WIN > (long long)P.n) return;
+    const K* xs = (s.final_buf ? P.B : P.A) + abs0;
+    const V* xv = PAIRS ? (s.final_buf ? P.Bv : P.Av) + abs0 : nullptr;
+    if ((reinterpret_cast<uintptr_t>(xs) & 15) || (PAIRS && (reinterpret_cast<uintptr_t>(xv) & 15)))
+      return;
+    fence_proxy_async();
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(S.bar + b)),
+                 "r"((uint32_t)DV_WIN_BYTES)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(S.win[b])),
+        "l"(xs), "r"((uint32_t)(WIN * sizeof(K))), "r"(smem_u32(S.bar + b))
+        : "memory");
+    if (PAIRS)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(S.win[b] + WIN * sizeof(K))),
+          "l"(xv), "r"((uint32_t)(WIN * 4)), "r"(smem_u32(S.bar + b))
+          : "memory");
+    S.misc[2 * b + 1] = 1;
+  }
+
+  // a bucket > N_d starting at segment index rb: find its end (gallop over
+  // the segment), queue it (Alg. 4 l.9-11)
+  static __device__ __noinline__ void divert_large(const Params<K>& P, const Seg& s, int rb,
+                                                   int known, int shift) {
+    const K* xs = (s.final_buf ? P.B : P.A) + s.start;
+    const K pre = xs[rb] >> shift;
+    const uint32_t len = s.len;
+    uint32_t lo = (uint32_t)max(known - 1, rb);  // index known to share the prefix
+    uint32_t hi = len;
+    uint32_t step = 64;
+    while (true) {  // gallop
+      const uint32_t probe = lo + step;
+      if (probe >= hi) break;
+      if ((xs[probe] >> shift) != pre) {
+        hi = probe;
+        break;
+      }
+      lo = probe;
+      step <<= 1;
+    }
+    while (hi - lo > 1) {  // first index in (lo, hi] with a different prefix
+      const uint32_t mid = (lo + hi) >> 1;
+      if ((xs[mid] >> shift) != pre)
+        hi = mid;
+      else
+        lo = mid;
+    }
+    push_bucket(P, s, s.start + (uint32_t)rb, hi - (uint32_t)rb);
+  }
+
+  // exact stable ranks of the bucket [bs, be) of the window, by one warp
+  static __device__ __noinline__ void rerank_exact(uint32_t sk_a, uint32_t order_a, int bs, int be) {
+    const int lane = threadIdx.x & 31;
+    for (int y = bs + lane; y < be; y += 32) {
+      const K ky = ldsk<K>(sk_a + sizeof(K) * y);
+      uint32_t r = 0;
+      for (int z = bs; z < be; ++z) {
+        const K kz = ldsk<K>(sk_a + sizeof(K) * z);
+        r += (kz < ky) || (kz == ky && z < y);
+      }
+      sts16(order_a + 2 * (bs + r), (uint32_t)y);
+    }
+  }
+
+  // highest set bit of the 96-bit word (hi:mid:lo), counted from bit 0 of lo,
+  // or -1 (branch-free selects)
+  static __device__ __forceinline__ int top_bit96(uint32_t hi, uint32_t mid, uint32_t lo) {
+    const int th = 95 - __clz(hi), tm = 63 - __clz(mid), tl = 31 - __clz(lo);
+    return hi ? th : (mid ? tm : tl);
+  }
+  // lowest set bit of the 96-bit word (hi:mid:lo), or 96
+  static __device__ __forceinline__ int low_bit96(uint32_t lo, uint32_t mid, uint32_t hi) {
+    const int bl = __ffs(lo) - 1, bmid = 31 + __ffs(mid), bh = 63 + __ffs(hi);
+    return lo ? bl : (mid ? bmid : (hi ? bh : 96));
+  }
+
+  // warp-wide exact re-rank of every bucket flagged in bmk (lanes' info)
+  static __device__ __noinline__ void rerank_flagged(uint32_t sk_a, uint32_t order_a, uint32_t bmk,
+                                                     uint32_t info, bool b) {
+    while (bmk) {
+      const uint32_t inf = __shfl_sync(0xffffffffu, info, __ffs(bmk) - 1);
+      bmk &= ~__ballot_sync(0xffffffffu, b && (info & 0xffffffu) == (inf & 0xffffffu));
+      rerank_exact(sk_a, order_a, inf & 0xfff, (inf >> 12) & 0xfff);
+    }
+  }
+
+  // Positions: warp w holds the contiguous range [w*WPW, (w+1)*WPW) of the
+  // window, 32 consecutive positions per step m.  The bucket-start ballot
+  // words of its own steps stay in registers; bucket bounds come from the
+  // lane's own word plus warp-uniform carries (last start before the step,
+  // first start after it), seeded by the two edge words of each neighbouring
+  // warp (shared memory).
+  template <int NT, bool LOSSY, bool EDGE>
+  static __device__ __forceinline__ void divert_window(const Params<K>& P, const Seg& s,
+                                                       const DivertSmem& S, uint32_t sk_a,
+                                                       uint32_t sv_a, int r0, int off,
+                                                       const Compo& comp) {
+    constexpr int NW = NT / 32, WPW = WIN / NW, DKPT = WPW / 32;
+    constexpr uint32_t KB = sizeof(K);
+    constexpr int NONE_LO = -(1 << 20), NONE_HI = 1 << 20;
+    static_assert(DKPT >= 2, "two edge words per warp");
     const int CH = (int)P.chunk;
     const int nd = (int)P.n_d;
-    const int W = 1 + CH + nd;  // == WIN
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int len = (int)s.len;
-    const K* xs = (s.final_buf ? P.B : P.A) + s.start;
-    const V* xv = PAIRS ? (s.final_buf ? P.Bv : P.Av) + s.start : nullptr;
-    const int shift = 8 * s.low;  // remaining bits R below the group (<= 56)
-    const int rlo = c0 - 1;       // segment index of window position 0
-    const K remmask = (K(1) << shift) - 1;
-
-    // load the window: one TMA bulk copy for an interior, 16-byte aligned window
-    const bool interior = rlo >= 0 && rlo + W <= len;
-    const bool tma = interior && !(reinterpret_cast<uintptr_t>(xs + rlo) & 15) &&
-                     !(PAIRS && (reinterpret_cast<uintptr_t>(xv + rlo) & 15));
-    if (tma) {
-      if (threadIdx.x == 0) {
-        fence_proxy_async();
-        const uint32_t bytes = WIN * sizeof(K) + (PAIRS ? WIN * 4 : 0);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(S.bar)),
-                     "r"(bytes)
-                     : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(sk)),
-            "l"(xs + rlo), "r"((uint32_t)(WIN * sizeof(K))), "r"(smem_u32(S.bar))
-            : "memory");
-        if (PAIRS)
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  smem_u32(sv)),
-              "l"(xv + rlo), "r"((uint32_t)(WIN * 4)), "r"(smem_u32(S.bar))
-              : "memory");
+    const int shift = 8 * s.low;
+    const int wbase = w * WPW;
+    const uint32_t cmp_a = smem_u32(S.cmp), order_a = smem_u32(S.order);
+    const uint32_t bm_a = smem_u32(S.bm);  // word index = position / 32 (zero words beyond both ends)
+    // ---- A: keys, bucket-start words
+    K key[DKPT];
+    uint32_t bw[DKPT];
+#pragma unroll
+    for (int m = 0; m < DKPT; ++m) {
+      const int i = wbase + 32 * m + lane;
+      key[m] = ldsk<K>(sk_a + KB * i);
+      const K kp = ldsk<K>(sk_a + KB * (i > 0 ? i - 1 : 0));
+      bool st = ((key[m] ^ kp) >> shift) != K(0);
+      if (m == 0) st |= i == 0;
+      if (EDGE) {
+        const int r = r0 + i;
+        st |= (unsigned)(r - 1) >= (unsigned)(len - 1);  // r <= 0 or r >= len
       }
-      mbar_wait(S.bar, parity);
-      parity ^= 1u;
-    } else {
-#pragma unroll 4
-      for (int m = 0; m < KPT; ++m) {
-        const int i = threadIdx.x + THREADS * m;
-        const int r = rlo + i;
-        const bool ok = r >= 0 && r < len;
-        sk[i] = ok ? xs[r] : K(0);
-        if (PAIRS) sv[i] = ok ? xv[r] : 0u;
+      bw[m] = __ballot_sync(0xffffffffu, st);
+    }
+    if (lane < 2) sts32(bm_a + 4 * (w * DKPT + lane), lane ? bw[1] : bw[0]);
+    if (lane == 2) sts32(bm_a + 4 * (w * DKPT + DKPT - 2), bw[DKPT - 2]);
+    if (lane == 3) sts32(bm_a + 4 * (w * DKPT + DKPT - 1), bw[DKPT - 1]);
+    if (nd > 64)  // generic N_d: every word through shared memory
+#pragma unroll
+      for (int m = 2; m < DKPT - 2; ++m)
+        if (lane == 0) sts32(bm_a + 4 * (w * DKPT + m), bw[m]);
+    {  // composites := +inf (the pad of every bucket's last group of four)
+      const uint4 inf4 = make_uint4(0x7c007c00u, 0x7c007c00u, 0x7c007c00u, 0x7c007c00u);
+      for (int x = threadIdx.x; x < DV_CMP / 8; x += NT) sts128(cmp_a + 16 * x, inf4);
+    }
+    __syncthreads();
+    // ---- B: bounds, composites of owned small-bucket keys, large starts
+    const uint32_t le = 0xffffffffu >> (31 - lane);
+    uint32_t info[DKPT];
+    uint32_t lg = 0;
+    if (nd <= 64) {
+      // first start after each step (backward carry), seeded by the next warp
+      int nxt[DKPT];
+      {
+        const uint32_t e0 = lds32(bm_a + 4 * (w * DKPT + DKPT)),
+                       e1 = lds32(bm_a + 4 * (w * DKPT + DKPT + 1));
+        int c = e0 ? wbase + WPW + __ffs(e0) - 1 : (e1 ? wbase + WPW + 31 + __ffs(e1) : NONE_HI);
+#pragma unroll
+        for (int m = DKPT - 1; m >= 0; --m) {
+          nxt[m] = c;
+          if (bw[m]) c = wbase + 32 * m + __ffs(bw[m]) - 1;
+        }
       }
+      // last start before each step (forward carry), seeded by the previous warp
+      const uint32_t f1 = lds32(bm_a + 4 * (w * DKPT - 1)), f2 = lds32(bm_a + 4 * (w * DKPT - 2));
+      int prv = f1 ? wbase - 1 - __clz(f1) : (f2 ? wbase - 33 - __clz(f2) : NONE_LO);
+#pragma unroll
+      for (int m = 0; m < DKPT; ++m) {
+        const int i = wbase + 32 * m + lane;
+        const int base = wbase + 32 * m;
+        const uint32_t lo = bw[m] & le, hi = bw[m] & ~le;
+        const int bs = lo ? base + 31 - __clz(lo) : prv;
+        const int be = hi ? base + __ffs(hi) - 1 : nxt[m];
+        if (bw[m]) prv = base + 31 - __clz(bw[m]);
+        bool own = bs >= off && bs < off + CH;
+        if (EDGE) own &= r0 + bs < len;
+        const bool small = be - bs <= nd;
+        info[m] = DV_NONE;
+        if (own && small) {
+          info[m] = (uint32_t)bs | ((uint32_t)be << 12);
+          sts16(cmp_a + 2 * (3 * bs + i), comp.template get<LOSSY>(key[m], (uint32_t)(i - bs)));
+        }
+        lg |= (uint32_t)(own && !small && i == bs) << m;
+      }
+    } else {  // generic N_d (up to 256): word-wise search in shared memory
       __syncthreads();
-    }
-    // bucket-start bitmask: bit i <=> a bucket (equal top-p prefix) starts at i
-#pragma unroll 4
-    for (int m = 0; m < KPT; ++m) {
-      const int i = threadIdx.x + THREADS * m;
-      const int r = rlo + i;
-      bool st = true;
-      if (r > 0 && r < len) st = (sk[i] >> shift) != (sk[i - 1] >> shift);
-      const uint32_t b = __ballot_sync(0xffffffffu, st);
-      if (lane == 0) bm[8 * m + w] = b;
-    }
-    __syncthreads();
-    // classify; composites of owned small buckets; queue owned large buckets.
-    // The bucket bounds of each of this thread's positions stay in registers.
-    uint32_t info[KPT];
+      const uint32_t* bmp = S.bm;
 #pragma unroll
-    for (int m = 0; m < KPT; ++m) {
-      const int i = threadIdx.x + THREADS * m;
-      const int r = rlo + i;
-      int bs, be;
-      if (FAST) {
-        bucket_bounds_fast(bm, i, bs, be);
-      } else {
-        bs = prev_set(bm, i, max(1, i - nd));
-        be = bs >= 1 ? next_set(bm, i, min(W - 1, bs + nd)) : -1;
-        if (be < 0) be = 1 << 20;
+      for (int m = 0; m < DKPT; ++m) {
+        const int i = wbase + 32 * m + lane;
+        int bs = prev_set(bmp, i, max(1, i - nd));
+        int be = bs >= 1 ? next_set(bmp, i, min(WIN - 1, bs + nd)) : -1;
+        if (be < 0) be = NONE_HI;
+        if (bs < 0) bs = NONE_LO;
+        bool own = bs >= off && bs < off + CH;
+        if (EDGE) own &= r0 + bs < len;
+        const bool small = be - bs <= nd;
+        info[m] = DV_NONE;
+        if (own && small) {
+          info[m] = (uint32_t)bs | ((uint32_t)be << 12);
+          sts16(cmp_a + 2 * (3 * bs + i), comp.template get<LOSSY>(key[m], (uint32_t)(i - bs)));
+        }
+        lg |= (uint32_t)(own && !small && i == bs) << m;
       }
-      info[m] = 0xffffffffu;
-      if (i >= 1 && r < len && bs >= 1 && bs <= CH) {  // owned
-        if (be - bs <= nd) {
-          info[m] = (uint32_t)bs | ((uint32_t)be << 16);
-          cmp[i] = ((CT)(sk[i] & remmask) << 8) | (CT)(i - bs);
-        } else if (i == bs) {
-          divert_large(P, s, sk, bm, xs, i, r, c0, W, len, shift);
+    }
+    if (lg)  // rare: queue the large buckets that start here
+      for (int m = 0; m < DKPT; ++m)
+        if ((lg >> m) & 1u) {
+          const int rb = r0 + wbase + 32 * m + lane;
+          divert_large(P, s, rb, rb + 1, shift);
+        }
+    __syncthreads();
+    // ---- C: ranks
+#pragma unroll
+    for (int m = 0; m < DKPT; ++m) {
+      const int i = wbase + 32 * m + lane;
+      const bool ok = info[m] != DV_NONE;
+      const int bs = ok ? (int)(info[m] & 0xfff) : 0;
+      const int ng = ok ? ((int)((info[m] >> 12) & 0xfff) - bs + 3) >> 2 : 0;
+      const uint32_t me = lds16(cmp_a + 2 * (ok ? 3 * bs + i : 0));
+      const __half2 me2 = __halves2half2(__ushort_as_half((unsigned short)me),
+                                         __ushort_as_half((unsigned short)me));
+      uint32_t pa = cmp_a + 8 * bs;
+      const uint32_t pe = pa + 8 * ng;
+      __half2 acc = __float2half2_rn(0.f);
+#pragma unroll 2
+      for (; pa < pe; pa += 8) {
+        const uint2 v = lds64v(pa);
+        acc = __hadd2(acc, __hlt2(*reinterpret_cast<const __half2*>(&v.x), me2));
+        acc = __hadd2(acc, __hlt2(*reinterpret_cast<const __half2*>(&v.y), me2));
+      }
+      const uint32_t rk = (uint32_t)__half2ushort_rz(__hadd(__low2half(acc), __high2half(acc)));
+      if (ok) {
+        sts16(order_a + 2 * (bs + rk), (uint32_t)i);
+        info[m] |= rk << 24;
+      }
+    }
+    // ---- D: tie check (lossy composites): a slot claimed by another key
+    if (LOSSY) {
+      __syncthreads();
+      uint32_t badm = 0;
+#pragma unroll
+      for (int m = 0; m < DKPT; ++m) {
+        const int i = wbase + 32 * m + lane;
+        if (info[m] != DV_NONE)
+          badm |= (uint32_t)(lds16(order_a + 2 * ((info[m] & 0xfff) + (info[m] >> 24))) != (uint32_t)i) << m;
+      }
+      if (__syncthreads_or(badm != 0)) {
+#pragma unroll
+        for (int m = 0; m < DKPT; ++m) {
+          const bool b = (badm >> m) & 1u;
+          const uint32_t bmk = __ballot_sync(0xffffffffu, b);
+          if (bmk) rerank_flagged(sk_a, order_a, bmk, info[m], b);
         }
       }
     }
     __syncthreads();
-    // rank inside the bucket; write each key straight to its slot in the
-    // caller's buffer (a permutation inside a ~16-key bucket: the warp's
-    // stores stay within a few 128-byte segments)
-    K* outk = P.A + s.start + rlo;
-    V* outv = P.Av + s.start + rlo;
+    // ---- E: coalesced write of every owned slot
+    K* outk = P.A + s.start + r0;
+    V* outv = P.Av + s.start + r0;
 #pragma unroll
-    for (int m = 0; m < KPT; ++m) {
-      if (info[m] != 0xffffffffu) {
-        const int i = threadIdx.x + THREADS * m;
-        const int bs = info[m] & 0xffff, bend = info[m] >> 16;
-        const CT me = cmp[i];
-        // count over [bs, bs + 4*ceil(len/4)), then take back the overrun
-        const int stop = bs + ((bend - bs + 3) & ~3);
-        uint32_t rk = 0;
-#pragma unroll 1
-        for (int x = bs; x < stop; x += 4) {
-          const CT a0 = cmp[x], a1 = cmp[x + 1], a2 = cmp[x + 2], a3 = cmp[x + 3];
-          rk += (uint32_t)(a0 < me) + (uint32_t)(a1 < me) + (uint32_t)(a2 < me) + (uint32_t)(a3 < me);
-        }
-        for (int x = bend; x < stop; ++x) rk -= (uint32_t)(cmp[x] < me);
-        outk[bs + rk] = sk[i];
-        if (PAIRS) outv[bs + rk] = sv[i];
+    for (int m = 0; m < DKPT; ++m) {
+      if (info[m] != DV_NONE) {
+        const int j = wbase + 32 * m + lane;
+        const uint32_t src = lds16(order_a + 2 * j);
+        outk[j] = ldsk<K>(sk_a + KB * src);
+        if (PAIRS) outv[j] = lds32(sv_a + 4 * src);
       }
     }
   }
 
-  static __device__ void divert(const Params<K>& P, uint32_t* sm) {
+  template <int NT>
+  static __device__ __forceinline__ void divert(const Params<K>& P, uint32_t* sm) {
     Ctl* c = P.ctl;
     const uint32_t total = c->total_chunks, nseg = c->nseg;
-    Seg* q = P.segq[c->cur];
+    const Seg* q = P.segq[c->cur];
     DivertSmem S;
-    S.sk = reinterpret_cast<K*>(sm);
-    S.cmp = reinterpret_cast<CT*>(S.sk + WIN);
-    S.sv = reinterpret_cast<V*>(S.cmp + WIN + 8);
-    uint32_t* bm0 = reinterpret_cast<uint32_t*>(PAIRS ? (void*)(S.sv + WIN) : (void*)S.sv);
+    char* base = reinterpret_cast<char*>(sm);
+    S.win[0] = base;
+    S.win[1] = base + DV_WIN_BYTES;
+    S.cmp = reinterpret_cast<uint16_t*>(base + 2 * DV_WIN_BYTES);
+    S.order = S.cmp + DV_CMP;
+    uint32_t* bm0 = reinterpret_cast<uint32_t*>(S.order + WIN);
     S.bm = bm0 + 4;
-    S.s_misc = S.bm + WIN / 32 + 4;
-    S.bar = reinterpret_cast<unsigned long long*>(S.s_misc + 8);
-    const int CH = (int)P.chunk;
-    const bool fast = P.n_d <= 64;
+    S.misc = S.bm + WIN / 32 + 4;
+    S.bar = reinterpret_cast<unsigned long long*>(S.misc + 4);
     if (threadIdx.x < 4) {
       bm0[threadIdx.x] = 0;
       S.bm[WIN / 32 + threadIdx.x] = 0;
     }
-    if (threadIdx.x < 8) S.cmp[WIN + threadIdx.x] = ~CT(0);  // overrun pad (taken back)
     if (threadIdx.x == 0) {
       mbar_init(S.bar, 1);
+      mbar_init(S.bar + 1, 1);
       fence_mbar_init();
+      divert_prefetch(P, q, nseg, total, blockIdx.x, S, 0);
     }
+    __syncthreads();
     uint32_t parity = 0;
-    for (uint32_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
-      if (threadIdx.x == 0) S.s_misc[0] = upper_index(nseg, ch, [&](uint32_t i) { return q[i].chunk0; });
-      __syncthreads();
-      const Seg s = q[S.s_misc[0]];
-      const int c0 = (int)(ch - s.chunk0) * CH;  // segment-relative chunk start
-      if (s.flags & (SEG_DONE | SEG_SKIP_DIVERT)) {
-      } else if (s.flags & SEG_COPY) {  // finished bucket left in B: copy out
-        const int c1 = min((int)s.len, c0 + CH);
-        for (int r = c0 + threadIdx.x; r < c1; r += THREADS) {
-          P.A[s.start + r] = P.B[s.start + r];
-          if (PAIRS) P.Av[s.start + r] = P.Bv[s.start + r];
+    int b = 0;
+    for (uint32_t ch = blockIdx.x; ch < total; ch += gridDim.x, b ^= 1) {
+      const Seg s = q[S.misc[2 * b]];
+      const bool tma = S.misc[2 * b + 1] != 0;
+      int c0, r0, off;
+      window_of(P, s, ch, c0, r0, off);
+      if (s.flags & (SEG_DONE | SEG_SKIP_DIVERT | SEG_COPY)) {
+        if (s.flags & SEG_COPY) {  // finished bucket left in B: copy out
+          const int c1 = min((int)s.len, c0 + (int)P.chunk);
+          for (int r = c0 + threadIdx.x; r < c1; r += blockDim.x) {
+            P.A[s.start + r] = P.B[s.start + r];
+            if (PAIRS) P.Av[s.start + r] = P.Bv[s.start + r];
+          }
         }
-      } else {
-        if (fast)
-          divert_chunk<true>(P, s, S, c0, parity);
-        else
-          divert_chunk<false>(P, s, S, c0, parity);
+        __syncthreads();
+        if (threadIdx.x == 0) divert_prefetch(P, q, nseg, total, ch + gridDim.x, S, b ^ 1);
+        __syncthreads();
+        continue;
       }
+      const uint32_t sk_a = smem_u32(S.win[b]);
+      const uint32_t sv_a = sk_a + WIN * sizeof(K);
+      if (tma) {
+        mbar_wait(S.bar + b, (parity >> b) & 1u);
+        parity ^= 1u << b;
+      } else {  // window at an array edge / unaligned: plain loads
+        K* wk = reinterpret_cast<K*>(S.win[b]);
+        V* wv = reinterpret_cast<V*>(S.win[b] + WIN * sizeof(K));
+        const K* xs = (s.final_buf ? P.B : P.A);
+        const V* xv = PAIRS ? (s.final_buf ? P.Bv : P.Av) : nullptr;
+        for (int i = threadIdx.x; i < WIN; i += blockDim.x) {
+          const long long a = (long long)s.start + r0 + i;
+          const bool ok = a >= 0 && a < (long long)P.n;
+          wk[i] = ok ? xs[a] : K(0);
+          if (PAIRS) wv[i] = ok ? xv[a] : 0u;
+        }
+        __syncthreads();
+      }
+      Compo comp;
+      comp.init(8 * s.low, (int)P.n_d);
+      const bool edge = r0 < 0 || r0 + WIN > (int)s.len;
+      if (comp.exact) {
+        if (edge) divert_window<NT, false, true>(P, s, S, sk_a, sv_a, r0, off, comp);
+        else      divert_window<NT, false, false>(P, s, S, sk_a, sv_a, r0, off, comp);
+      } else {
+        if (edge) divert_window<NT, true, true>(P, s, S, sk_a, sv_a, r0, off, comp);
+        else      divert_window<NT, true, false>(P, s, S, sk_a, sv_a, r0, off, comp);
+      }
+      // the other buffer was last read before this window's first barrier
+      if (threadIdx.x == 0) divert_prefetch(P, q, nseg, total, ch + gridDim.x, S, b ^ 1);
       __syncthreads();
-      fence_proxy_async();  // generic smem accesses before the next TMA into the window
+      fence_proxy_async();
     }
   }
 
