@@ -264,13 +264,18 @@ __device__ __forceinline__ void warp_rank(uint32_t (&io)[N], uint32_t* whist) {
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     const uint32_t d = io[j];
-    uint32_t peers = 0xffffffffu;
+    // digit bit b moved to the sign position: its ballot, xor the spread of
+    // the lane's own bit, marks the lanes that differ in that bit
+    constexpr int NB = FULL ? 8 : 9;
+    const int x = (int)(d << (32 - NB));
+    uint32_t diff = 0;
 #pragma unroll
-    for (int b = 0; b < (FULL ? 8 : 9); ++b) {
-      const bool set = (d >> b) & 1u;
-      const uint32_t v = __ballot_sync(0xffffffffu, set);
-      peers &= set ? v : ~v;
+    for (int b = 0; b < NB; ++b) {
+      const int xb = x << b;
+      const uint32_t v = __ballot_sync(0xffffffffu, xb < 0);
+      diff |= v ^ (uint32_t)(xb >> 31);
     }
+    const uint32_t peers = ~diff;
     const uint32_t leader = __ffs(peers) - 1;
     uint32_t old = 0;
     if (lane == leader && (FULL || d < 256)) old = atomicAdd(&whist[d], __popc(peers));
