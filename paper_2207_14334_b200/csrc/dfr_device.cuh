@@ -20,7 +20,7 @@ constexpr int THREADS = 256;             // one CTA = 8 warps
 constexpr int WARPS = THREADS / 32;
 constexpr int KPT = 16;                  // keys per thread per tile
 constexpr int TILE = THREADS * KPT;      // 4096 keys per tile (hist / deal)
-constexpr int WIN = 2048;                // diversion window (keys) per CTA
+constexpr int WIN = 1024;                // diversion window (keys) per CTA
 constexpr int MID_CAP = 4096;            // C: buckets N_d < s <= C finish on-chip
 constexpr int MAX_ND = 256;              // composite index uses 8 bits
 constexpr int MAX_PASSES = 4;            // top passes per group (p <= 3 for n < 2^30)

@@ -673,7 +673,7 @@ struct Phases {
   static constexpr uint16_t H_INF = 0x7c00;   // +inf: never below a composite
   static constexpr uint16_t H_BASE = 0x0400;  // smallest positive normal fp16
   static constexpr uint32_t DV_NONE = 0xffffffffu;
-  static constexpr int DV_NT = 256;           // threads of the stand-alone divert kernel
+  static constexpr int DV_NT = 128;           // threads of the stand-alone divert kernel
   static constexpr size_t DV_WIN_BYTES = WIN * sizeof(K) + (PAIRS ? WIN * 4 : 0);
   static constexpr int DV_CMP = 4 * WIN + 64;  // halves
 
