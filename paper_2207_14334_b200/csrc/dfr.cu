@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(THREADS) k_plan2(const __grid_constant__ Param
 }
 
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(256, 3) k_scatter(const __grid_constant__ Params<K> P, int j) {
+__global__ void __launch_bounds__(Phases<K, PAIRS>::SC_NT, 3) k_scatter(const __grid_constant__ Params<K> P, int j) {
   extern __shared__ __align__(16) uint32_t sm[];
   Phases<K, PAIRS>::template scatter<Phases<K, PAIRS>::SC_NT>(P, j, sm);
 }

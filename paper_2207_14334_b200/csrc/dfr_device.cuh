@@ -257,30 +257,44 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
 // broadcasts the old value.  whist (256 u32) must be zero on entry.
 // io[j]: in = digit (256 marks an invalid item, only when !FULL);
 // out = digit | rank << 16.
+template <bool FULL>
+__device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
+  // digit bit b moved to the sign position: its ballot, xor the spread of
+  // the lane's own bit, marks the lanes that differ in that bit
+  constexpr int NB = FULL ? 8 : 9;
+  const int x = (int)(d << (32 - NB));
+  uint32_t diff = 0;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int xb = x << b;
+    const uint32_t v = __ballot_sync(0xffffffffu, xb < 0);
+    diff |= v ^ (uint32_t)(xb >> 31);
+  }
+  return ~diff;
+}
+
 template <int N, bool FULL>
 __device__ __forceinline__ void warp_rank(uint32_t (&io)[N], uint32_t* whist) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
+  // peer masks of G items first (independent ballot chains), then their
+  // counter updates in item order
+  constexpr int G = 4;
+  static_assert(N % G == 0, "items per group");
 #pragma unroll
-  for (int j = 0; j < N; ++j) {
-    const uint32_t d = io[j];
-    // digit bit b moved to the sign position: its ballot, xor the spread of
-    // the lane's own bit, marks the lanes that differ in that bit
-    constexpr int NB = FULL ? 8 : 9;
-    const int x = (int)(d << (32 - NB));
-    uint32_t diff = 0;
+  for (int j0 = 0; j0 < N; j0 += G) {
+    uint32_t peers[G];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int xb = x << b;
-      const uint32_t v = __ballot_sync(0xffffffffu, xb < 0);
-      diff |= v ^ (uint32_t)(xb >> 31);
+    for (int g = 0; g < G; ++g) peers[g] = warp_peers<FULL>(io[j0 + g]);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t d = io[j0 + g];
+      const uint32_t leader = __ffs(peers[g]) - 1;
+      uint32_t old = 0;
+      if (lane == leader && (FULL || d < 256)) old = atomicAdd(&whist[d], __popc(peers[g]));
+      old = __shfl_sync(0xffffffffu, old, leader);
+      io[j0 + g] = d | ((old + __popc(peers[g] & lt)) << 16);
     }
-    const uint32_t peers = ~diff;
-    const uint32_t leader = __ffs(peers) - 1;
-    uint32_t old = 0;
-    if (lane == leader && (FULL || d < 256)) old = atomicAdd(&whist[d], __popc(peers));
-    old = __shfl_sync(0xffffffffu, old, leader);
-    io[j] = d | ((old + __popc(peers & lt)) << 16);
   }
 }
 

@@ -33,7 +33,7 @@ struct Phases {
 
   // ------------------------------------------------------------ smem sizes
   static constexpr size_t SMEM_HIST = WARPS * MAX_PASSES * 256 * 4 + 64;
-  static constexpr int SCATTER_HDR_WORDS = (256 / 32 + 1) * 256 + 256 + 32;
+  static constexpr int SCATTER_HDR_WORDS = (512 / 32 + 1) * 256 + 256 + 32;  // up to 16 warps
   static constexpr size_t SMEM_SCATTER =
       SCATTER_HDR_WORDS * 4 + 2 * TILE * sizeof(K) + (PAIRS ? 2 * TILE * 4 : 0);
   // 2 windows (+ values) | fp16 composites | order | bitmask, misc, mbarriers
