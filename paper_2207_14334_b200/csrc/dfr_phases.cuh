@@ -33,7 +33,10 @@ struct Phases {
 
   // ------------------------------------------------------------ smem sizes
   static constexpr size_t SMEM_HIST = WARPS * MAX_PASSES * 256 * 4 + 64;
-  static constexpr int SCATTER_HDR_WORDS = (512 / 32 + 1) * 256 + 256 + 32;  // up to 16 warps
+  // The deal kernel runs SC_NT threads per CTA over tiles of TILE keys
+  // (3 CTAs/SM: 24 warps hide the look-back and load latencies best)
+  static constexpr int SC_NT = 256;
+  static constexpr int SCATTER_HDR_WORDS = (SC_NT / 32 + 1) * 256 + 256 + 32;
   static constexpr size_t SMEM_SCATTER =
       SCATTER_HDR_WORDS * 4 + 2 * TILE * sizeof(K) + (PAIRS ? 2 * TILE * 4 : 0);
   // 2 windows (+ values) | fp16 composites | order | bitmask, misc, mbarriers
@@ -344,10 +347,6 @@ struct Phases {
     return s.buf ^ (before & 1u);
   }
 
-  // The deal kernel runs SC_NT threads per CTA (16 warps) over tiles of TILE
-  // keys: SC_KPT keys per thread.  32 warps per SM hide the look-back and
-  // load latencies better than 24 and halve each warp's ranking chain.
-  static constexpr int SC_NT = 256;
 
   // rank, publish, reorder, look back, write out — one staged tile
   template <int SC_NT, bool FULL, class Hook>
