@@ -354,7 +354,8 @@ struct Phases {
                                                    const Seg& s, int j,
                                                    uint32_t t, uint32_t lt, uint32_t cnt, int dg,
                                                    uint32_t* status, K* sk, V* sv, uint32_t* whist,
-                                                   int* s_dst, uint32_t* s_warp, K* dst, V* dstv) {
+                                                   int* s_dst, uint32_t* s_warp, K* dst, V* dstv,
+                                                   uint32_t bstart) {
     constexpr int SC_W = SC_NT / 32;
     constexpr int SC_KPT = TILE / SC_NT;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -434,7 +435,6 @@ struct Phases {
         }
         st_relaxed(status + (size_t)t * 256 + dd, FLAG_INC | (excl + run));
       }
-      const uint32_t bstart = P.hist[(size_t)(s.hist_off + j) * 256 + dd];
       // run offset of the digit relative to the tile's local offsets, mod 2^32
       s_dst[dd] = (int)(s.start + bstart + excl - lstart);
     }
@@ -528,6 +528,10 @@ struct Phases {
       claim_tile(P, j, q, nseg, total, ti, kb0, vb0, &bar[0]);
     }
     uint32_t phases = 0;  // mbarrier parity per buffer
+    // the segment record and its bucket-offset row are re-read only when a
+    // tile of another segment comes up (level 0: once per CTA)
+    uint32_t cur_si = ~0u, bstart = 0;
+    Seg s;
 
     for (int it = 0;; ++it) {
       const int cb = it & 1;
@@ -535,7 +539,13 @@ struct Phases {
       __syncthreads();  // ti[cb] visible; whist zeroed; the other buffer is free
       const uint32_t t = ti[cb * 4 + 0];
       if (t >= total) break;
-      const Seg s = q[ti[cb * 4 + 1]];
+      const uint32_t si = ti[cb * 4 + 1];
+      if (si != cur_si) {
+        cur_si = si;
+        s = q[si];
+        if (threadIdx.x < 256 && pass_active(s, j))
+          bstart = P.hist[(size_t)(s.hist_off + j) * 256 + threadIdx.x];
+      }
       const bool tma = ti[cb * 4 + 2] != 0;
       K* sk = kb0 + cb * TILE;
       V* sv = vb0 + cb * TILE;
@@ -568,10 +578,10 @@ struct Phases {
       }
       if (cnt == (uint32_t)TILE)
         deal_tile<SC_NT, true>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist, s_dst, s_warp,
-                               dst, dstv);
+                               dst, dstv, bstart);
       else
         deal_tile<SC_NT, false>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist, s_dst,
-                                s_warp, dst, dstv);
+                                s_warp, dst, dstv, bstart);
       fence_proxy_async();  // generic smem accesses before a later TMA into this buffer
     }
     // every claimed ticket < total was processed, so no bulk copy is in flight here
