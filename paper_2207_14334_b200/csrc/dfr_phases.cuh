@@ -411,18 +411,19 @@ struct Phases {
     }
     if (dig_thread) {
       uint32_t excl = 0;
-      if (lt > 0) {  // decoupled look-back, up to 4 predecessors per round trip
+      if (lt > 0) {  // decoupled look-back, up to LB predecessors per round trip
         int tt = (int)t - 1;
         const int t0 = (int)s.tile0;  // publishes FLAG_INC, so the walk ends there
         while (true) {
-          uint32_t v[4];
+          constexpr int LB = 8;  // predecessors per look-back round trip
+          uint32_t v[LB];
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
+          for (int k = 0; k < LB; ++k)
             v[k] = (tt - k >= t0) ? ld_relaxed(status + (size_t)(tt - k) * 256 + dd) : FLAG_INC;
           int k = 0;
           bool done = false;
 #pragma unroll
-          for (; k < 4; ++k) {
+          for (; k < LB; ++k) {
             if ((v[k] >> 30) == 0) break;  // not published yet: retry from here
             excl += v[k] & VAL_MASK;
             if (v[k] & FLAG_INC) {
