@@ -65,6 +65,14 @@ typedef struct dfr_config {
                                 caller: events[2i] / events[2i+1] are recorded on `stream`
                                 before / after phase i (see DFR_PHASE_*); a phase that does
                                 not run records both back to back.  No synchronisation. */
+  uint32_t fused_last_pass; /* 0 (default): separate last deal + diversion kernels.
+                               1: a large top call (p = 3, keys only, n >= 2^27,
+                               n_d <= 64) runs its last deal and the diversion of the
+                               resulting buckets as ONE kernel over tiles made of whole
+                               runs of the two lower group digits (same output; the
+                               plain path is taken on the device when a run is longer
+                               than a tile).  Measured slower on B200:
+                               the diversion is ALU-bound, fusing saves only bytes. */
 } dfr_config;
 
 /* Phases timed through dfr_config.phase_events. */
@@ -87,6 +95,7 @@ typedef struct dfr_stats {
   uint64_t global_segments;   /* buckets > 4096 recursed through the global queue */
   uint32_t levels;            /* recursion levels executed after level 0 */
   uint32_t overflow;          /* device queue overflow flags (0 = none; non-zero = bug) */
+  uint32_t fused;             /* 1: the top call ran the fused last deal + diversion */
 } dfr_stats;
 
 /*

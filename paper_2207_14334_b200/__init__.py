@@ -41,14 +41,15 @@ class DfrError(RuntimeError):
 
 class Config(ctypes.Structure):
     _fields_ = [("n_d", ctypes.c_uint32), ("skip_trivial_passes", ctypes.c_uint32),
-                ("phase_events", ctypes.POINTER(ctypes.c_void_p))]
+                ("phase_events", ctypes.POINTER(ctypes.c_void_p)),
+                ("fused_last_pass", ctypes.c_uint32)]
 
 
 class Stats(ctypes.Structure):
     _fields_ = [("level0_p", ctypes.c_uint32), ("level0_passes_run", ctypes.c_uint32),
                 ("level0_large", ctypes.c_uint64), ("mid_buckets", ctypes.c_uint64),
                 ("global_segments", ctypes.c_uint64), ("levels", ctypes.c_uint32),
-                ("overflow", ctypes.c_uint32)]
+                ("overflow", ctypes.c_uint32), ("fused", ctypes.c_uint32)]
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f, _ in self._fields_}
@@ -121,9 +122,10 @@ def _dev_tensor(t, widths):
     return t
 
 
-def _cfg(n_d, skip_trivial, events=None):
-    """events: None or a sequence of 2*len(PHASES) torch.cuda.Event(enable_timing=True)."""
-    c = Config(int(n_d), 1 if skip_trivial else 0, None)
+def _cfg(n_d, skip_trivial, events=None, fused=False):
+    """events: None or a sequence of 2*len(PHASES) torch.cuda.Event(enable_timing=True).
+    fused=True asks for the fused last deal + diversion (dfr_config.fused_last_pass)."""
+    c = Config(int(n_d), 1 if skip_trivial else 0, None, 1 if fused else 0)
     if events is not None:
         arr = (ctypes.c_void_p * len(events))(*[int(e.cuda_event) for e in events])
         c._keep = arr
@@ -135,32 +137,34 @@ def launch_counter() -> int:
     return int(lib().dfr_launch_counter())
 
 
-def sort_u32(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, events=None):
+def sort_u32(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, events=None,
+             fused=False):
     """In-place ascending sort of a contiguous CUDA tensor of 32-bit keys (bit
     patterns read as uint32)."""
     _dev_tensor(keys, (4,))
     st = Stats() if stats else None
     rc = lib().dfr_sort_u32_ex(keys.data_ptr(), keys.numel(), _stream(stream),
-                               ctypes.byref(_cfg(n_d, skip_trivial, events)),
+                               ctypes.byref(_cfg(n_d, skip_trivial, events, fused)),
                                ctypes.byref(st) if st is not None else None)
     _check(rc, "dfr_sort_u32")
     return st.as_dict() if st is not None else None
 
 
-def sort_u64(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, events=None):
+def sort_u64(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, events=None,
+             fused=False):
     """In-place ascending sort of a contiguous CUDA tensor of 64-bit keys (bit
     patterns read as uint64; int64 tensors are accepted as raw storage)."""
     _dev_tensor(keys, (8,))
     st = Stats() if stats else None
     rc = lib().dfr_sort_u64_ex(keys.data_ptr(), keys.numel(), _stream(stream),
-                               ctypes.byref(_cfg(n_d, skip_trivial, events)),
+                               ctypes.byref(_cfg(n_d, skip_trivial, events, fused)),
                                ctypes.byref(st) if st is not None else None)
     _check(rc, "dfr_sort_u64")
     return st.as_dict() if st is not None else None
 
 
 def sort_pairs_u32(keys, vals, *, n_d=64, skip_trivial=True, stream=None, stats=False,
-                   events=None):
+                   events=None, fused=False):
     """Stable in-place sort of (uint32 key, uint32 value) pairs held in two
     contiguous CUDA tensors of equal length."""
     _dev_tensor(keys, (4,))
@@ -169,7 +173,7 @@ def sort_pairs_u32(keys, vals, *, n_d=64, skip_trivial=True, stream=None, stats=
         raise DfrError("keys and vals differ in length")
     st = Stats() if stats else None
     rc = lib().dfr_sort_pairs_u32_ex(keys.data_ptr(), vals.data_ptr(), keys.numel(),
-                                     _stream(stream), ctypes.byref(_cfg(n_d, skip_trivial, events)),
+                                     _stream(stream), ctypes.byref(_cfg(n_d, skip_trivial, events, fused)),
                                      ctypes.byref(st) if st is not None else None)
     _check(rc, "dfr_sort_pairs_u32")
     return st.as_dict() if st is not None else None

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
     s.start = 0;
     s.len = n;
     s.hi = P.D - 1;
-    s.buf = 0;
+    s.buf = P.fuse ? 1u : 0u;  // fused level 0: the histogram kernel copies A to B first
     P.segq[1][0] = s;
   }
   __syncthreads();
@@ -90,10 +90,28 @@ __global__ void __launch_bounds__(Phases<K, PAIRS>::SC_NT, 3) k_scatter(const __
   Phases<K, PAIRS>::template scatter<Phases<K, PAIRS>::SC_NT>(P, j, sm);
 }
 
+// the middle pass of a fused level 0: the deal plus the joint histogram
+template <class K>
+__global__ void __launch_bounds__(Phases<K, false>::SC_NT, 3) k_scatter_fh(const __grid_constant__ Params<K> P, int j) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  Phases<K, false>::template scatter<Phases<K, false>::SC_NT, true>(P, j, sm);
+}
+
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(Phases<K, PAIRS>::DV_NT, 8) k_divert(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
   Phases<K, PAIRS>::template divert<Phases<K, PAIRS>::DV_NT>(P, sm);
+}
+
+template <class K, bool PAIRS>
+__global__ void __launch_bounds__(1024) k_fplan(const __grid_constant__ Params<K> P) {
+  Phases<K, PAIRS>::fplan(P);
+}
+
+template <class K, bool PAIRS>
+__global__ void __launch_bounds__(Phases<K, PAIRS>::FNT, 2) k_fused(const __grid_constant__ Params<K> P) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  Phases<K, PAIRS>::fused(P, sm);
 }
 
 template <class K, bool PAIRS>
@@ -175,7 +193,7 @@ struct PhaseEv {  // optional caller-provided events around each phase
 
 struct Dev {
   int sms = 0;
-  int occ_hist = 0, occ_scatter = 0, occ_divert = 0, occ_mid = 0, occ_levels = 0;
+  int occ_hist = 0, occ_scatter = 0, occ_divert = 0, occ_mid = 0, occ_levels = 0, occ_fused = 0;
 };
 
 template <class K, bool PAIRS>
@@ -207,6 +225,9 @@ static cudaError_t get_dev(Dev& out) {
     setup((const void*)k_init<K, PAIRS>, 64, &d.occ_hist);
     setup((const void*)k_hist<K, PAIRS>, Ph::SMEM_HIST, &d.occ_hist);
     setup((const void*)k_plan2<K, PAIRS>, 64, &d.occ_mid);
+    if (err == cudaSuccess && !PAIRS)
+      err = cudaFuncSetAttribute((const void*)k_scatter_fh<K>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_SCATTER);
     if (err == cudaSuccess) {  // the deal runs 512-thread CTAs
       err = cudaFuncSetAttribute((const void*)k_scatter<K, PAIRS>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_SCATTER);
@@ -222,6 +243,13 @@ static cudaError_t get_dev(Dev& out) {
             &d.occ_divert, (const void*)k_divert<K, PAIRS>, Ph::DV_NT, Ph::SMEM_DIVERT);
     }
     setup((const void*)k_mid<K, PAIRS>, Ph::SMEM_MID, &d.occ_mid);
+    if (err == cudaSuccess) {  // fused last pass: FNT-thread CTAs
+      err = cudaFuncSetAttribute((const void*)k_fused<K, PAIRS>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_FUSED);
+      if (err == cudaSuccess)
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_fused, (const void*)k_fused<K, PAIRS>,
+                                                            Ph::FNT, Ph::SMEM_FUSED);
+    }
     setup((const void*)k_levels<K, PAIRS>, Ph::SMEM_LEVEL, &d.occ_levels);
     devs[dev] = d;
     errs[dev] = err;
@@ -233,11 +261,12 @@ static cudaError_t get_dev(Dev& out) {
 static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t b_keys, b_vals, ctl, segq0, segq1, midq, hist, status, total;
+  size_t b_keys, b_vals, ctl, segq0, segq1, midq, hist, status, fh, ftiles, total;
   size_t max_segs, mid_cap, hist_rows, tiles_max;
 };
 
-static Layout make_layout(size_t n, int kb, int vb, uint32_t n_d, int min_passes = 1) {
+static Layout make_layout(size_t n, int kb, int vb, uint32_t n_d, int min_passes = 1,
+                          bool fuse = false) {
   Layout L{};
   L.max_segs = n / (MID_CAP + 1) + 2;
   L.mid_cap = n / (n_d + 1) + 2;
@@ -261,6 +290,8 @@ static Layout make_layout(size_t n, int kb, int vb, uint32_t n_d, int min_passes
   int passes = est_top_passes(n, n_d);  // no group of any level has more passes
   passes = passes < min_passes ? min_passes : (passes > MAX_PASSES ? MAX_PASSES : passes);
   L.status = take((size_t)passes * L.tiles_max * 256 * 4);
+  L.fh = fuse ? take(65536 * 4) : 0;      // joint histogram of the two low group digits
+  L.ftiles = fuse ? take(65536 * 8) : 0;  // run-aligned tiles of the fused pass
   L.total = off;
   return L;
 }
@@ -281,6 +312,8 @@ static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals,
   P.hist = reinterpret_cast<uint32_t*>(ws + L.hist);
   P.status = reinterpret_cast<uint32_t*>(ws + L.status);
   P.status_stride = L.tiles_max * 256;
+  P.H = L.fh ? reinterpret_cast<uint32_t*>(ws + L.fh) : nullptr;
+  P.ftiles = L.ftiles ? reinterpret_cast<uint2*>(ws + L.ftiles) : nullptr;
   P.max_segs = (uint32_t)L.max_segs;
   P.mid_cap = (uint32_t)L.mid_cap;
   P.hist_rows = (uint32_t)L.hist_rows;
@@ -291,12 +324,14 @@ static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals,
   return P;
 }
 
-static int cfg_nd(const dfr_config* cfg, uint32_t* n_d, uint32_t* skip) {
+static int cfg_nd(const dfr_config* cfg, uint32_t* n_d, uint32_t* skip, uint32_t* nofuse) {
   *n_d = DFR_DEFAULT_ND;
   *skip = 1;
+  *nofuse = 1;
   if (cfg) {
     *n_d = cfg->n_d ? cfg->n_d : DFR_DEFAULT_ND;
     *skip = cfg->skip_trivial_passes ? 1 : 0;
+    *nofuse = cfg->fused_last_pass ? 0 : 1;
   }
   if (*n_d < 8 || *n_d > (uint32_t)MAX_ND) return DFR_ERR_INVALID;
   return DFR_OK;
@@ -306,8 +341,8 @@ template <class K, bool PAIRS>
 static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const dfr_config* cfg,
                      dfr_stats* stats) {
   using Ph = Phases<K, PAIRS>;
-  uint32_t n_d, skip;
-  if (cfg_nd(cfg, &n_d, &skip) != DFR_OK) return DFR_ERR_INVALID;
+  uint32_t n_d, skip, nofuse;
+  if (cfg_nd(cfg, &n_d, &skip, &nofuse) != DFR_OK) return DFR_ERR_INVALID;
   if (stats) memset(stats, 0, sizeof(*stats));
   if (n <= 1) return DFR_OK;
   if (!keys || (PAIRS && !vals)) return DFR_ERR_INVALID;
@@ -323,13 +358,19 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
   if (get_dev<K, PAIRS>(dv) != cudaSuccess) return DFR_ERR_CUDA;
   cudaGetLastError();
 
-  const Layout L = make_layout(n, sizeof(K), PAIRS ? 4 : 0, n_d);
+  int p0 = est_top_passes(n, n_d);
+  if (p0 > (int)sizeof(K)) p0 = (int)sizeof(K);
+  // fused last pass (Phases::fused): large keys-only top calls with 3 group digits
+  const bool fuse = !PAIRS && !nofuse && p0 == 3 && n_d <= 64 && n >= ((size_t)1 << 27) &&
+                    n > (size_t)MID_CAP;
+  const Layout L = make_layout(n, sizeof(K), PAIRS ? 4 : 0, n_d, 1, fuse);
   char* ws = nullptr;
   if (cudaMallocAsync(reinterpret_cast<void**>(&ws), L.total, st) != cudaSuccess) {
     cudaGetLastError();
     return DFR_ERR_ALLOC;
   }
   Params<K> P = make_params<K>(ws, L, keys, vals, PAIRS, n_d, skip, n);
+  P.fuse = fuse ? 1u : 0u;
   const uint32_t nn = (uint32_t)n;
   const int sms = dv.sms;
   const PhaseEv pe{cfg ? cfg->phase_events : nullptr, st};
@@ -342,8 +383,6 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
     pe.end(DFR_PHASE_MID);
     g_launches += 2;
   } else {
-    int p0 = est_top_passes(n, n_d);
-    if (p0 > (int)sizeof(K)) p0 = (int)sizeof(K);
     const uint32_t tiles = (nn + TILE - 1) / TILE;
     pe.begin(DFR_PHASE_HIST);
     k_init<K, PAIRS><<<1, THREADS, 64, st>>>(P, nn);
@@ -360,7 +399,16 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
         continue;
       }
       pe.begin(DFR_PHASE_SCATTER0 + j);
-      k_scatter<K, PAIRS><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER, st>>>(P, j);
+      if (fuse && j == 2) {  // run-aligned tiles, then the fused last deal + diversion
+        k_fplan<K, PAIRS><<<1, 1024, 0, st>>>(P);
+        const int g_f = sms * std::max(1, dv.occ_fused);
+        k_fused<K, PAIRS><<<g_f, Ph::FNT, Ph::SMEM_FUSED, st>>>(P);
+        g_launches += 2;
+      }
+      if (fuse && j == 1 && !PAIRS)
+        k_scatter_fh<K><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER, st>>>(P, j);
+      else
+        k_scatter<K, PAIRS><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER, st>>>(P, j);  // no-op when fused
       pe.end(DFR_PHASE_SCATTER0 + j);
     }
     const uint32_t chunks = (nn + P.chunk - 1) / P.chunk;
@@ -399,6 +447,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
       stats->global_segments = h.global_segments;
       stats->levels = h.levels_run;
       stats->overflow = h.overflow;
+      stats->fused = h.fused_ok;
     }
   }
   if (cudaFreeAsync(ws, st) != cudaSuccess && rc == DFR_OK) rc = DFR_ERR_CUDA;

@@ -72,6 +72,10 @@ struct Ctl {
   unsigned long long global_segments;
   uint32_t level0_p, level0_run;
   uint32_t levels_run, max_p;
+  uint32_t fused_ok;            // level 0 ran the fused last pass (plan kernel's verdict)
+  uint32_t fused_tiles;         // run-aligned tiles of the fused pass
+  uint32_t fticket;             // dynamic tile ticket of the fused pass
+  uint32_t fused_pad;
 };
 
 template <class K>
@@ -92,6 +96,9 @@ struct Params {
   uint32_t n_d;         // diversion threshold N_d
   uint32_t chunk;       // diversion chunk = WIN - 16/sizeof(K) - n_d
   uint32_t n;           // elements of the whole array
+  uint32_t fuse;        // level 0 may fuse its last deal with the diversion (host decision)
+  uint32_t* H;          // joint histogram of the group's two low digits [d_mid][d_low] (fuse)
+  uint2* ftiles;        // run-aligned tiles of the fused pass: (segment offset, length)
   uint32_t skip_trivial;
   int D;                // digits per key
 };

@@ -177,9 +177,11 @@ struct Phases {
 
   // one tile: diff mask + counts of the NP group digits
   template <int NP>
+  // cp != nullptr: the tile is also copied to cp (fused level 0 starts its
+  // passes from the scratch buffer, so that the fused last pass lands in A)
   static __device__ __forceinline__ void hist_tile(const K* tp, uint32_t cnt, K kref, int low,
-                                                   uint32_t shw, unsigned long long& diff) {
-    if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0) {
+                                                   uint32_t shw, unsigned long long& diff, K* cp) {
+    if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0 && (reinterpret_cast<uintptr_t>(cp) & 15) == 0) {
       const uint32_t nv = cnt / VEC;
       const uint4* vp = reinterpret_cast<const uint4*>(tp);
       constexpr int U = 4;  // 4 independent 16-byte loads in flight per thread
@@ -188,6 +190,9 @@ struct Phases {
         uint4 x[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) x[u] = __ldg(vp + vb + u * THREADS + threadIdx.x);
+        if (cp)
+#pragma unroll
+          for (int u = 0; u < U; ++u) reinterpret_cast<uint4*>(cp)[vb + u * THREADS + threadIdx.x] = x[u];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const K* kk = reinterpret_cast<const K*>(&x[u]);
@@ -202,6 +207,7 @@ struct Phases {
         const uint32_t v = vb + threadIdx.x;
         const bool ok = v < nv;
         uint4 x = ok ? __ldg(vp + v) : make_uint4(0, 0, 0, 0);
+        if (cp && ok) reinterpret_cast<uint4*>(cp)[v] = x;
         const K* kk = reinterpret_cast<const K*>(&x);
 #pragma unroll
         for (int e = 0; e < VEC; ++e) {
@@ -213,6 +219,7 @@ struct Phases {
         const uint32_t ii = nv * VEC + threadIdx.x;
         const bool ok = ii < cnt;
         K k = ok ? tp[ii] : K(0);
+        if (cp && ok) cp[ii] = k;
         if (ok) diff |= (unsigned long long)(k ^ kref);
         count_key<NP>(shw, k, ok, low);
       }
@@ -221,6 +228,7 @@ struct Phases {
         const uint32_t i = ib + threadIdx.x;
         const bool ok = i < cnt;
         K k = ok ? tp[i] : K(0);
+        if (cp && ok) cp[i] = k;
         if (ok) diff |= (unsigned long long)(k ^ kref);
         count_key<NP>(shw, k, ok, low);
       }
@@ -236,6 +244,13 @@ struct Phases {
     const uint32_t total = c->total_tiles, nseg = c->nseg;
     if (total == 0) return;
     Seg* q = P.segq[c->cur];
+    const bool fcopy = P.fuse && c->level == 0;
+    if (fcopy) {  // fused level 0: clear the joint histogram and the fused pass's status rows
+      const uint32_t gid = blockIdx.x * THREADS + threadIdx.x, gsz = gridDim.x * THREADS;
+      for (uint32_t x = gid; x < 65536u; x += gsz) P.H[x] = 0;
+      uint32_t* st2 = P.status + 2 * P.status_stride;
+      for (size_t x = (size_t)total * 256 + gid; x < (size_t)65536 * 256; x += gsz) st2[x] = 0;
+    }
     const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
     const uint32_t t0 = blockIdx.x * per;
     const uint32_t t1 = min(total, t0 + per);
@@ -259,14 +274,15 @@ struct Phases {
       const uint32_t cnt = min((uint32_t)TILE, s.len - lt * TILE);
       for (uint32_t j = 0; j < s.p; ++j)
         P.status[j * P.status_stride + (size_t)t * 256 + threadIdx.x] = 0;
-      const K* src = s.buf ? P.B : P.A;
+      const K* src = (s.buf && !fcopy) ? P.B : P.A;  // fused level 0: the input is still in A
       const K kref = src[s.start];
       const K* tp = src + base;
+      K* cp = fcopy ? P.B + base : nullptr;
       switch (s.p) {
-        case 1: hist_tile<1>(tp, cnt, kref, s.low, shw, diff); break;
-        case 2: hist_tile<2>(tp, cnt, kref, s.low, shw, diff); break;
-        case 3: hist_tile<3>(tp, cnt, kref, s.low, shw, diff); break;
-        default: hist_tile<4>(tp, cnt, kref, s.low, shw, diff); break;
+        case 1: hist_tile<1>(tp, cnt, kref, s.low, shw, diff, cp); break;
+        case 2: hist_tile<2>(tp, cnt, kref, s.low, shw, diff, cp); break;
+        case 3: hist_tile<3>(tp, cnt, kref, s.low, shw, diff, cp); break;
+        default: hist_tile<4>(tp, cnt, kref, s.low, shw, diff, cp); break;
       }
     }
     hist_flush(P, q, si, s, sh, diff);
@@ -349,7 +365,7 @@ struct Phases {
 
 
   // rank, publish, reorder, look back, write out — one staged tile
-  template <int SC_NT, bool FULL, class Hook>
+  template <int SC_NT, bool FULL, bool FUSEH, class Hook>
   static __device__ __forceinline__ void deal_tile(const Hook& after_lookback, const Params<K>& P,
                                                    const Seg& s, int j,
                                                    uint32_t t, uint32_t lt, uint32_t cnt, int dg,
@@ -375,6 +391,17 @@ struct Phases {
       if (FULL || idx < cnt) red_add_shared(tc_s + 4 * dr[jj], 1u);  // tile histogram
     }
     __syncthreads();
+    if (FUSEH) {  // joint histogram [this digit][digit below] for the fused last pass
+      const uint32_t lo0 = digit_of(sk[0], s.low), lo1 = digit_of(sk[cnt - 1], s.low);
+      if (lo0 == lo1) {  // input sorted by the digit below: the whole tile shares it
+        if (threadIdx.x < 256 && tcount[threadIdx.x])
+          atomicAdd(&P.H[threadIdx.x * 256 + lo0], tcount[threadIdx.x]);
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < SC_KPT; ++jj)
+          if (dr[jj] < 256) atomicAdd(&P.H[dr[jj] * 256 + digit_of(key[jj], s.low)], 1u);
+      }
+    }
     // publish the tile aggregate as early as possible: successors' look-backs
     // then rarely wait for this tile
     const uint32_t dd = threadIdx.x;
@@ -507,12 +534,14 @@ struct Phases {
   // inclusive prefix: the load and the ticket round trip overlap the current
   // tile's write-out, and tickets are still claimed in (nearly) completion
   // order, which keeps the look-back of later tiles short.
-  template <int SC_NT>
+  // FUSEH: the middle pass of a fused level 0 also counts the joint histogram
+  template <int SC_NT, bool FUSEH = false>
   static __device__ void scatter(const Params<K>& P, int j, uint32_t* sm) {
     constexpr int SC_W = SC_NT / 32;
     Ctl* c = P.ctl;
     const uint32_t total = c->total_tiles, nseg = c->nseg;
     if ((uint32_t)j >= c->max_p) return;  // no segment of this level has pass j
+    if (P.fuse && j == 2 && c->level == 0 && *(volatile uint32_t*)&c->fused_ok) return;  // fused pass did it
     const Seg* q = P.segq[c->cur];
     uint32_t* whist = sm;                                         // SC_W*256
     int* s_dst = reinterpret_cast<int*>(whist + (SC_W + 1) * 256);  // 256 (after tcount)
@@ -578,11 +607,11 @@ struct Phases {
         __syncthreads();
       }
       if (cnt == (uint32_t)TILE)
-        deal_tile<SC_NT, true>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist, s_dst, s_warp,
-                               dst, dstv, bstart);
+        deal_tile<SC_NT, true, FUSEH>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist, s_dst,
+                                      s_warp, dst, dstv, bstart);
       else
-        deal_tile<SC_NT, false>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist, s_dst,
-                                s_warp, dst, dstv, bstart);
+        deal_tile<SC_NT, false, FUSEH>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist, s_dst,
+                                       s_warp, dst, dstv, bstart);
       fence_proxy_async();  // generic smem accesses before a later TMA into this buffer
     }
     // every claimed ticket < total was processed, so no bulk copy is in flight here
@@ -1016,6 +1045,7 @@ struct Phases {
   template <int NT>
   static __device__ __forceinline__ void divert(const Params<K>& P, uint32_t* sm) {
     Ctl* c = P.ctl;
+    if (P.fuse && c->level == 0 && *(volatile uint32_t*)&c->fused_ok) return;  // done by the fused pass
     const uint32_t total = c->total_chunks, nseg = c->nseg;
     const Seg* q = P.segq[c->cur];
     DivertSmem S;
@@ -1091,6 +1121,289 @@ struct Phases {
       if (threadIdx.x == 0) divert_prefetch(P, q, nseg, total, ch + gridDim.x, S, b ^ 1);
       __syncthreads();
       fence_proxy_async();
+    }
+  }
+
+  // ============================================================ fused last pass
+  // Level 0 with p = 3 group digits (lo, mid, hi) on large inputs: after the
+  // passes on lo and mid the data is sorted by (mid, lo), so every run of
+  // equal (mid, lo) -- an "s-run" -- is contiguous, and the buckets of the
+  // level (Alg. 4 l.8: equal top-3-digit prefix) are exactly the keys of one
+  // s-run that share digit hi.  A tile made of one whole s-run therefore
+  // holds its buckets complete: the last deal (Alg. 4 l.6, digit hi) and the
+  // diversion of its small buckets (l.10-14) run on the tile in one kernel,
+  // and the keys leave shared memory already in their final order.  The
+  // s-runs come from the joint histogram H[mid][lo] counted during the pass
+  // on mid.  Buckets > N_d are queued for recursion (l.11) as in the
+  // diversion kernel.  The plan kernel falls back (fused_ok = 0) to the plain
+  // deal + diversion when an s-run exceeds the tile or a pass was skipped.
+  static constexpr int FNT = 384, FKPT = 12, FNW = FNT / 32;
+  static constexpr int FT_MAX = FNT * FKPT;          // 4608 keys per tile
+  static constexpr int F_CMP = FT_MAX + 3 * 256 + 64;  // composite halves
+  struct FHdr {  // words
+    static constexpr int WHIST = 0, TC = FNW * 256, LST = TC + 256, SDST = LST + 256,
+                         BST = SDST + 256, SWARP = BST + 256, MISC = SWARP + 16, WORDS = MISC + 16;
+  };
+  static constexpr size_t SMEM_FUSED =
+      (size_t)FHdr::WORDS * 4 + FT_MAX * sizeof(K) + F_CMP * 2 + FT_MAX * 2;
+
+  // one CTA of 1024 threads: s-run offsets and the tile list from H
+  static __device__ void fplan(const Params<K>& P) {
+    Ctl* c = P.ctl;
+    __shared__ uint32_t s_w[32], s_w2[32], s_m[32];
+    const Seg s = P.segq[c->cur][0];
+    const bool eligible = P.fuse && c->level == 0 && c->nseg == 1 && s.p == 3 &&
+                          (s.flags & (0xfu | SEG_SKIP_DIVERT | SEG_COPY | SEG_DONE)) == 0;
+    if (!eligible) {
+      if (threadIdx.x == 0) c->fused_ok = 0;
+      return;
+    }
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const uint32_t* h = P.H + 64 * t;
+    uint32_t sum = 0, mx = 0, nz = 0;
+    for (int k = 0; k < 64; ++k) {
+      const uint32_t x = h[k];
+      sum += x;
+      mx = max(mx, x);
+      nz += x != 0;
+    }
+    uint32_t a = sum, b = nz;  // inclusive warp scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t ya = __shfl_up_sync(0xffffffffu, a, o), yb = __shfl_up_sync(0xffffffffu, b, o);
+      if (lane >= o) {
+        a += ya;
+        b += yb;
+      }
+    }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 31) {
+      s_w[w] = a;
+      s_w2[w] = b;
+    }
+    if (lane == 0) s_m[w] = mx;
+    __syncthreads();
+    uint32_t pa = 0, pb = 0, tot = 0, ntl = 0, gmx = 0;
+    for (int e = 0; e < 32; ++e) {
+      if (e < w) {
+        pa += s_w[e];
+        pb += s_w2[e];
+      }
+      tot += s_w[e];
+      ntl += s_w2[e];
+      gmx = max(gmx, s_m[e]);
+    }
+    const bool ok = gmx <= (uint32_t)FT_MAX && tot == s.len;
+    if (ok) {
+      uint32_t pos = pa + a - sum, ti = pb + b - nz;
+      for (int k = 0; k < 64; ++k) {
+        const uint32_t x = h[k];
+        if (x) P.ftiles[ti++] = make_uint2(pos, x);
+        pos += x;
+      }
+    }
+    if (t == 0) {
+      c->fused_ok = ok ? 1u : 0u;
+      c->fused_tiles = ntl;
+      c->fticket = 0;
+    }
+  }
+
+  static __device__ void fused(const Params<K>& P, uint32_t* sm) {
+    Ctl* c = P.ctl;
+    if (!*(volatile uint32_t*)&c->fused_ok) return;
+    const uint32_t ntiles = c->fused_tiles;
+    const Seg s = P.segq[c->cur][0];
+    const int j = 2, dg = s.low + 2;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nd = (int)P.n_d;
+    uint32_t* hdr = sm;
+    uint32_t* whist = hdr + FHdr::WHIST;
+    uint32_t* mywh = whist + w * 256;
+    uint32_t* tcount = hdr + FHdr::TC;
+    uint32_t* lstart = hdr + FHdr::LST;
+    int* s_dst = reinterpret_cast<int*>(hdr + FHdr::SDST);
+    uint32_t* bst = hdr + FHdr::BST;
+    uint32_t* s_warp = hdr + FHdr::SWARP;
+    uint32_t* misc = hdr + FHdr::MISC;
+    K* sk = reinterpret_cast<K*>(hdr + ((FHdr::WORDS + 3) & ~3));
+    uint16_t* cmp = reinterpret_cast<uint16_t*>(sk + FT_MAX);
+    uint16_t* order = cmp + F_CMP;
+    const uint32_t sk_a = smem_u32(sk), cmp_a = smem_u32(cmp), order_a = smem_u32(order);
+    const uint32_t tc_s = smem_u32(tcount);
+    uint32_t* status = P.status + (size_t)j * P.status_stride;
+    const K* src = (src_buf(s, j) ? P.B : P.A) + s.start;
+    K* dst = src_buf(s, j) ? P.A : P.B;
+    Compo comp;
+    comp.init(8 * s.low, nd);
+    if (threadIdx.x < 256) bst[threadIdx.x] = P.hist[(size_t)(s.hist_off + j) * 256 + threadIdx.x];
+
+    while (true) {
+      // ---- claim, clear, load
+      if (threadIdx.x == 0) misc[0] = atomicAdd(&c->fticket, 1u);
+      for (int e = lane; e < 256; e += 32) mywh[e] = 0;
+      if (threadIdx.x < 256) tcount[threadIdx.x] = 0;
+      {
+        const uint4 inf4 = make_uint4(0x7c007c00u, 0x7c007c00u, 0x7c007c00u, 0x7c007c00u);
+        for (int x = threadIdx.x; x < F_CMP / 8; x += FNT) sts128(cmp_a + 16 * x, inf4);
+      }
+      __syncthreads();
+      const uint32_t t = misc[0];
+      if (t >= ntiles) break;
+      const uint2 td = P.ftiles[t];
+      const int len = (int)td.y;
+      const K* tsrc = src + td.x;
+#pragma unroll 4
+      for (int i = threadIdx.x; i < len; i += FNT) sk[i] = tsrc[i];
+      __syncthreads();
+      // ---- deal on digit dg (as deal_tile)
+      K key[FKPT];
+      uint32_t dr[FKPT];
+#pragma unroll
+      for (int jj = 0; jj < FKPT; ++jj) {
+        const int idx = w * 32 * FKPT + jj * 32 + lane;
+        const bool ok = idx < len;
+        key[jj] = ok ? sk[idx] : K(0);
+        dr[jj] = ok ? digit_of(key[jj], dg) : 256u;
+        if (ok) red_add_shared(tc_s + 4 * dr[jj], 1u);
+      }
+      __syncthreads();
+      const uint32_t dd = threadIdx.x;
+      const bool dig = dd < 256;
+      const uint32_t cntd = dig ? tcount[dd] : 0u;
+      if (dig) st_relaxed(status + (size_t)t * 256 + dd, (t == 0 ? FLAG_INC : FLAG_AGG) | cntd);
+      warp_rank<FKPT, false>(dr, mywh);
+      uint32_t tot;
+      const uint32_t lst = block_excl_scan<FNT>(cntd, s_warp, &tot);  // syncs: ranks done
+      if (dig) {
+        lstart[dd] = lst;
+        uint32_t acc = lst;
+#pragma unroll
+        for (int e = 0; e < FNW; ++e) {
+          const uint32_t x = whist[e * 256 + dd];
+          whist[e * 256 + dd] = acc;
+          acc += x;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int jj = 0; jj < FKPT; ++jj) {
+        const uint32_t dgt = dr[jj] & 0xffffu;
+        if (dgt < 256) sk[mywh[dgt] + (dr[jj] >> 16)] = key[jj];
+      }
+      if (dig) {
+        uint32_t excl = 0;
+        if (t > 0) {
+          int tt = (int)t - 1;
+          while (true) {
+            constexpr int LB = 8;
+            uint32_t v[LB];
+#pragma unroll
+            for (int k = 0; k < LB; ++k)
+              v[k] = (tt - k >= 0) ? ld_relaxed(status + (size_t)(tt - k) * 256 + dd) : FLAG_INC;
+            int k = 0;
+            bool done = false;
+#pragma unroll
+            for (; k < LB; ++k) {
+              if ((v[k] >> 30) == 0) break;
+              excl += v[k] & VAL_MASK;
+              if (v[k] & FLAG_INC) {
+                done = true;
+                break;
+              }
+            }
+            if (done) break;
+            tt -= k;
+          }
+          st_relaxed(status + (size_t)t * 256 + dd, FLAG_INC | (excl + cntd));
+        }
+        s_dst[dd] = (int)(s.start + bst[dd] + excl - lst);
+      }
+      __syncthreads();
+      // ---- diversion of the tile's buckets (digit runs of the reordered tile)
+      uint32_t info[FKPT];
+#pragma unroll
+      for (int m = 0; m < FKPT; ++m) {
+        const int i = threadIdx.x + FNT * m;
+        info[m] = DV_NONE;
+        if (i < len) {
+          const K k = ldsk<K>(sk_a + sizeof(K) * i);
+          const uint32_t d = digit_of(k, dg);
+          const int bs = (int)lstart[d], sz = (int)tcount[d], idx = i - bs;
+          info[m] = d | ((uint32_t)idx << 8);
+          if (sz > 1 && sz <= nd) {
+            const int pst = (bs + 3 * (int)d + 3) & ~3;
+            sts16(cmp_a + 2 * (pst + idx), comp(k, (uint32_t)idx));
+          } else if (sz > nd && idx == 0) {
+            push_bucket(P, s, (uint32_t)s_dst[d] + (uint32_t)bs, (uint32_t)sz);
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int m = 0; m < FKPT; ++m) {
+        const int i = threadIdx.x + FNT * m;
+        if (info[m] != DV_NONE) {
+          const uint32_t d = info[m] & 255u;
+          const int idx = (int)(info[m] >> 8);
+          const int bs = (int)lstart[d], sz = (int)tcount[d];
+          uint32_t rk = (uint32_t)idx;
+          if (sz > 1 && sz <= nd) {
+            const int pst = (bs + 3 * (int)d + 3) & ~3;
+            const uint32_t me = lds16(cmp_a + 2 * (pst + idx));
+            const __half2 me2 = __halves2half2(__ushort_as_half((unsigned short)me),
+                                               __ushort_as_half((unsigned short)me));
+            uint32_t pa = cmp_a + 2 * pst;
+            const uint32_t pe = pa + 8 * ((sz + 3) >> 2);
+            __half2 acc = __float2half2_rn(0.f);
+#pragma unroll 2
+            for (; pa < pe; pa += 8) {
+              const uint2 v = lds64v(pa);
+              acc = __hadd2(acc, __hlt2(*reinterpret_cast<const __half2*>(&v.x), me2));
+              acc = __hadd2(acc, __hlt2(*reinterpret_cast<const __half2*>(&v.y), me2));
+            }
+            rk = (uint32_t)__half2ushort_rz(__hadd(__low2half(acc), __high2half(acc)));
+          }
+          sts16(order_a + 2 * (bs + (int)rk), (uint32_t)i);
+          info[m] = d | ((uint32_t)idx << 8) | (rk << 21);  // idx < 2^13, rk < 2^11
+        }
+      }
+      if (!comp.exact) {  // tie check: a slot claimed by another key
+        __syncthreads();
+        uint32_t badm = 0;
+#pragma unroll
+        for (int m = 0; m < FKPT; ++m) {
+          const int i = threadIdx.x + FNT * m;
+          if (info[m] != DV_NONE) {
+            const uint32_t d = info[m] & 255u;
+            const uint32_t bs = lstart[d];
+            badm |= (uint32_t)(lds16(order_a + 2 * (bs + (info[m] >> 21))) != (uint32_t)i) << m;
+          }
+        }
+        if (__syncthreads_or(badm != 0)) {
+#pragma unroll
+          for (int m = 0; m < FKPT; ++m) {
+            const bool b = (badm >> m) & 1u;
+            uint32_t bmk = __ballot_sync(0xffffffffu, b);
+            const uint32_t d = info[m] & 255u;
+            while (bmk) {
+              const uint32_t dl = __shfl_sync(0xffffffffu, d, __ffs(bmk) - 1);
+              bmk &= ~__ballot_sync(0xffffffffu, b && d == dl);
+              rerank_exact(sk_a, order_a, (int)lstart[dl], (int)(lstart[dl] + tcount[dl]));
+            }
+          }
+        }
+      }
+      __syncthreads();
+      // ---- write every slot in final order
+#pragma unroll
+      for (int m = 0; m < FKPT; ++m) {
+        const int i = threadIdx.x + FNT * m;
+        if (info[m] != DV_NONE) {
+          const uint32_t srcpos = lds16(order_a + 2 * i);
+          dst[(uint32_t)s_dst[info[m] & 255u] + (uint32_t)i] = ldsk<K>(sk_a + sizeof(K) * srcpos);
+        }
+      }
     }
   }
 
