@@ -862,7 +862,7 @@ struct Phases {
     while (bmk) {
       const uint32_t inf = __shfl_sync(0xffffffffu, info, __ffs(bmk) - 1);
       bmk &= ~__ballot_sync(0xffffffffu, b && (info & 0xffffffu) == (inf & 0xffffffu));
-      rerank_exact(sk_a, order_a, inf & 0xfff, (inf >> 12) & 0xfff);
+      rerank_exact(sk_a, order_a, inf & 0xfff, (inf & 0xfff) + ((inf >> 12) & 0x1ff));
     }
   }
 
@@ -889,6 +889,7 @@ struct Phases {
     const int wbase = w * WPW;
     const uint32_t cmp_a = smem_u32(S.cmp), order_a = smem_u32(S.order);
     const uint32_t bm_a = smem_u32(S.bm);  // word index = position / 32 (zero words beyond both ends)
+    const K pmask = (K)(~K(0) << shift);  // the group prefix bits of a key
     // ---- A: keys, bucket-start words
     K key[DKPT];
     uint32_t bw[DKPT];
@@ -897,7 +898,7 @@ struct Phases {
       const int i = wbase + 32 * m + lane;
       key[m] = ldsk<K>(sk_a + KB * i);
       const K kp = ldsk<K>(sk_a + KB * (i > 0 ? i - 1 : 0));
-      bool st = ((key[m] ^ kp) >> shift) != K(0);
+      bool st = ((key[m] ^ kp) & pmask) != K(0);
       if (m == 0) st |= i == 0;
       if (EDGE) {
         const int r = r0 + i;
@@ -919,7 +920,10 @@ struct Phases {
     __syncthreads();
     // ---- B: bounds, composites of owned small-bucket keys, large starts
     const uint32_t le = 0xffffffffu >> (31 - lane);
-    uint32_t info[DKPT];
+    uint32_t info[DKPT];      // bs | size << 12 | rank << 24, or DV_NONE
+    uint32_t mev[DKPT / 2];   // the composites of the lane's positions, two per word
+#pragma unroll
+    for (int m = 0; m < DKPT / 2; ++m) mev[m] = 0;
     uint32_t lg = 0;
     if (nd <= 64) {
       // first start after each step (backward carry), seeded by the next warp
@@ -950,8 +954,10 @@ struct Phases {
         const bool small = be - bs <= nd;
         info[m] = DV_NONE;
         if (own && small) {
-          info[m] = (uint32_t)bs | ((uint32_t)be << 12);
-          sts16(cmp_a + 2 * (3 * bs + i), comp.template get<LOSSY>(key[m], (uint32_t)(i - bs)));
+          info[m] = (uint32_t)bs | ((uint32_t)(be - bs) << 12);
+          const uint32_t c16 = comp.template get<LOSSY>(key[m], (uint32_t)(i - bs));
+          mev[m >> 1] |= c16 << (16 * (m & 1));
+          sts16(cmp_a + 2 * (3 * bs + i), c16);
         }
         lg |= (uint32_t)(own && !small && i == bs) << m;
       }
@@ -970,8 +976,10 @@ struct Phases {
         const bool small = be - bs <= nd;
         info[m] = DV_NONE;
         if (own && small) {
-          info[m] = (uint32_t)bs | ((uint32_t)be << 12);
-          sts16(cmp_a + 2 * (3 * bs + i), comp.template get<LOSSY>(key[m], (uint32_t)(i - bs)));
+          info[m] = (uint32_t)bs | ((uint32_t)(be - bs) << 12);
+          const uint32_t c16 = comp.template get<LOSSY>(key[m], (uint32_t)(i - bs));
+          mev[m >> 1] |= c16 << (16 * (m & 1));
+          sts16(cmp_a + 2 * (3 * bs + i), c16);
         }
         lg |= (uint32_t)(own && !small && i == bs) << m;
       }
@@ -989,8 +997,8 @@ struct Phases {
       const int i = wbase + 32 * m + lane;
       const bool ok = info[m] != DV_NONE;
       const int bs = ok ? (int)(info[m] & 0xfff) : 0;
-      const int ng = ok ? ((int)((info[m] >> 12) & 0xfff) - bs + 3) >> 2 : 0;
-      const uint32_t me = lds16(cmp_a + 2 * (ok ? 3 * bs + i : 0));
+      const int ng = ok ? (int)(((info[m] >> 12) & 0x1ff) + 3) >> 2 : 0;
+      const uint32_t me = (mev[m >> 1] >> (16 * (m & 1))) & 0xffffu;
       const __half2 me2 = __halves2half2(__ushort_as_half((unsigned short)me),
                                          __ushort_as_half((unsigned short)me));
       uint32_t pa = cmp_a + 8 * bs;
@@ -1071,8 +1079,16 @@ struct Phases {
     __syncthreads();
     uint32_t parity = 0;
     int b = 0;
+    uint32_t cur_si = ~0u;  // the segment record and composite plan change rarely
+    Seg s;
+    Compo comp;
     for (uint32_t ch = blockIdx.x; ch < total; ch += gridDim.x, b ^= 1) {
-      const Seg s = q[S.misc[2 * b]];
+      const uint32_t si = S.misc[2 * b];
+      if (si != cur_si) {
+        cur_si = si;
+        s = q[si];
+        comp.init(8 * s.low, (int)P.n_d);
+      }
       const bool tma = S.misc[2 * b + 1] != 0;
       int c0, r0, off;
       window_of(P, s, ch, c0, r0, off);
@@ -1107,8 +1123,6 @@ struct Phases {
         }
         __syncthreads();
       }
-      Compo comp;
-      comp.init(8 * s.low, (int)P.n_d);
       const bool edge = r0 < 0 || r0 + WIN > (int)s.len;
       if (comp.exact) {
         if (edge) divert_window<NT, false, true>(P, s, S, sk_a, sv_a, r0, off, comp);
