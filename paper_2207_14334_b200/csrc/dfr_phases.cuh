@@ -1090,6 +1090,9 @@ struct Phases {
         comp.init(8 * s.low, (int)P.n_d);
       }
       const bool tma = S.misc[2 * b + 1] != 0;
+      // the next window goes to the other buffer, free since the previous
+      // window's closing barrier: its load overlaps this whole window
+      if (threadIdx.x == 0) divert_prefetch(P, q, nseg, total, ch + gridDim.x, S, b ^ 1);
       int c0, r0, off;
       window_of(P, s, ch, c0, r0, off);
       if (s.flags & (SEG_DONE | SEG_SKIP_DIVERT | SEG_COPY)) {
@@ -1100,8 +1103,6 @@ struct Phases {
             if (PAIRS) P.Av[s.start + r] = P.Bv[s.start + r];
           }
         }
-        __syncthreads();
-        if (threadIdx.x == 0) divert_prefetch(P, q, nseg, total, ch + gridDim.x, S, b ^ 1);
         __syncthreads();
         continue;
       }
@@ -1131,10 +1132,7 @@ struct Phases {
         if (edge) divert_window<NT, true, true>(P, s, S, sk_a, sv_a, r0, off, comp);
         else      divert_window<NT, true, false>(P, s, S, sk_a, sv_a, r0, off, comp);
       }
-      // the other buffer was last read before this window's first barrier
-      if (threadIdx.x == 0) divert_prefetch(P, q, nseg, total, ch + gridDim.x, S, b ^ 1);
-      __syncthreads();
-      fence_proxy_async();
+      __syncthreads();  // window buffer, composites and order free
     }
   }
 
