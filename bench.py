@@ -109,6 +109,24 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
 
 
+def reduce_max_ms(ms, world, device="cpu"):
+    """Timing of a multi-rank run: the MAX of the ranks' device-measured times
+    (all ranks get it).  world == 1: unchanged."""
+    if world == 1:
+        return ms
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_value(n, world, steps, ms):
+    """Whole-job throughput in Gkeys/s: every rank sorts its own n keys per step
+    (replicas, weak scaling), all ranks together in the max-over-ranks time."""
+    return world * n * steps / (ms / 1e3) / 1e9
+
+
 def workload(case, n):
     import datagen
     c = datagen.CASES[case]
@@ -246,9 +264,7 @@ def run_dfr(args, rank, world, local_rank):
     launches = dfr.launch_counter() - l0
     if world > 1:
         dist.barrier()
-        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
+    elapsed = reduce_max_ms(elapsed, world, dev)
 
     # per-phase device times (CUDA events recorded by the library on this stream)
     phase_ms = {}
@@ -261,7 +277,7 @@ def run_dfr(args, rank, world, local_rank):
     verified = bool(datagen.is_sorted(out_h) and datagen.fingerprint(out_h) == fp_in)
     del out_h
 
-    value = world * n * K / (elapsed / 1e3) / 1e9
+    value = job_value(n, world, K, elapsed)
     ms_per_step = elapsed / K
     peak, peak_src = peak_hbm()
 
@@ -340,12 +356,8 @@ def run_e2e(args, dfr, torch, dev, keys_h, vals_h, tdt, n, kb, vb, world):
         step()
     b.record(s)
     torch.cuda.synchronize()
-    ms = a.elapsed_time(b)
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    return {"value": world * n * K / (ms / 1e3) / 1e9, "unit": UNIT,
+    ms = reduce_max_ms(a.elapsed_time(b), world, dev)
+    return {"value": job_value(n, world, K, ms), "unit": UNIT,
             "h2d_bytes_per_step": n * (kb + vb), "d2h_bytes_per_step": n * (kb + vb),
             "ms_per_step": ms / K}
 
