@@ -85,9 +85,9 @@ __global__ void __launch_bounds__(THREADS) k_plan2(const __grid_constant__ Param
 }
 
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(Phases<K, PAIRS>::SC_NT, 3) k_scatter(const __grid_constant__ Params<K> P, int j) {
+__global__ void __launch_bounds__(Phases<K, PAIRS>::SC_NT, 4) k_scatter(const __grid_constant__ Params<K> P, int j) {
   extern __shared__ __align__(16) uint32_t sm[];
-  Phases<K, PAIRS>::template scatter<Phases<K, PAIRS>::SC_NT>(P, j, sm);
+  Phases<K, PAIRS>::template scatter<Phases<K, PAIRS>::SC_NT, false, true>(P, j, sm);
 }
 
 // the middle pass of a fused level 0: the deal plus the joint histogram
@@ -228,12 +228,12 @@ static cudaError_t get_dev(Dev& out) {
     if (err == cudaSuccess && !PAIRS)
       err = cudaFuncSetAttribute((const void*)k_scatter_fh<K>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_SCATTER);
-    if (err == cudaSuccess) {  // the deal runs 512-thread CTAs
+    if (err == cudaSuccess) {  // the deal (one tile buffer + permutation)
       err = cudaFuncSetAttribute((const void*)k_scatter<K, PAIRS>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_SCATTER);
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_SCATTER_P);
       if (err == cudaSuccess)
         err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &d.occ_scatter, (const void*)k_scatter<K, PAIRS>, Ph::SC_NT, Ph::SMEM_SCATTER);
+            &d.occ_scatter, (const void*)k_scatter<K, PAIRS>, Ph::SC_NT, Ph::SMEM_SCATTER_P);
     }
     if (err == cudaSuccess) {  // the diversion runs DV_NT-thread CTAs
       err = cudaFuncSetAttribute((const void*)k_divert<K, PAIRS>,
@@ -408,7 +408,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
       if (fuse && j == 1 && !PAIRS)
         k_scatter_fh<K><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER, st>>>(P, j);
       else
-        k_scatter<K, PAIRS><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER, st>>>(P, j);  // no-op when fused
+        k_scatter<K, PAIRS><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER_P, st>>>(P, j);  // no-op when fused
       pe.end(DFR_PHASE_SCATTER0 + j);
     }
     const uint32_t chunks = (nn + P.chunk - 1) / P.chunk;
@@ -489,7 +489,7 @@ static int stage_impl(const K* in, const uint32_t* vin, K* out, uint32_t* vout, 
     k_plan2<K, PAIRS><<<1, THREADS, 64, st>>>(P);
     DFR_CHECK_LAUNCH("k_plan2(stage)");
     const int g_sc = (int)std::min<uint32_t>(tiles, (uint32_t)(dv.sms * std::max(1, dv.occ_scatter)));
-    k_scatter<K, PAIRS><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER, st>>>(P, 0);
+    k_scatter<K, PAIRS><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER_P, st>>>(P, 0);
     DFR_CHECK_LAUNCH("k_scatter(stage)");
   }
   cudaError_t e = cudaGetLastError();

@@ -39,6 +39,9 @@ struct Phases {
   static constexpr int SCATTER_HDR_WORDS = (SC_NT / 32 + 1) * 256 + 256 + 32;
   static constexpr size_t SMEM_SCATTER =
       SCATTER_HDR_WORDS * 4 + 2 * TILE * sizeof(K) + (PAIRS ? 2 * TILE * 4 : 0);
+  // PERM deal: header | permutation | one tile
+  static constexpr size_t SMEM_SCATTER_P =
+      SCATTER_HDR_WORDS * 4 + TILE * 2 + TILE * sizeof(K) + (PAIRS ? TILE * 4 : 0);
   // 2 windows (+ values) | fp16 composites | order | bitmask, misc, mbarriers
   static constexpr size_t SMEM_DIVERT = 2 * (WIN * sizeof(K) + (PAIRS ? WIN * 4 : 0)) +
                                         (4 * WIN + 64) * 2 + WIN * 2 + (WIN / 32 + 12) * 4 + 16 + 16;
@@ -365,13 +368,17 @@ struct Phases {
 
 
   // rank, publish, reorder, look back, write out — one staged tile
-  template <int SC_NT, bool FULL, bool FUSEH, class Hook>
+  // PERM: the keys are not held in registers through the rank; the tile is
+  // reordered as a permutation of positions (u16, `perm`) and the write-out
+  // gathers keys through it — 32 fewer registers per thread (u64), which lets
+  // 4 CTAs share an SM.
+  template <int SC_NT, bool FULL, bool FUSEH, bool PERM, class Hook>
   static __device__ __forceinline__ void deal_tile(const Hook& after_lookback, const Params<K>& P,
                                                    const Seg& s, int j,
                                                    uint32_t t, uint32_t lt, uint32_t cnt, int dg,
                                                    uint32_t* status, K* sk, V* sv, uint32_t* whist,
                                                    int* s_dst, uint32_t* s_warp, K* dst, V* dstv,
-                                                   uint32_t bstart) {
+                                                   uint32_t bstart, uint16_t* perm) {
     constexpr int SC_W = SC_NT / 32;
     constexpr int SC_KPT = TILE / SC_NT;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -386,7 +393,7 @@ struct Phases {
     for (int jj = 0; jj < SC_KPT; ++jj) {
       const uint32_t idx = w * 32 * SC_KPT + jj * 32 + lane;
       key[jj] = sk[idx];
-      if (PAIRS) val[jj] = sv[idx];
+      if (PAIRS && !PERM) val[jj] = sv[idx];
       dr[jj] = (FULL || idx < cnt) ? digit_of(key[jj], dg) : 256u;
       if (FULL || idx < cnt) red_add_shared(tc_s + 4 * dr[jj], 1u);  // tile histogram
     }
@@ -432,8 +439,12 @@ struct Phases {
       const uint32_t dgt = dr[jj] & 0xffffu;
       if (FULL || dgt < 256) {
         const uint32_t pos = mywh[dgt] + (dr[jj] >> 16);
-        sk[pos] = key[jj];
-        if (PAIRS) sv[pos] = val[jj];
+        if (PERM) {
+          perm[pos] = (uint16_t)(w * 32 * SC_KPT + jj * 32 + lane);
+        } else {
+          sk[pos] = key[jj];
+          if (PAIRS) sv[pos] = val[jj];
+        }
       }
     }
     if (dig_thread) {
@@ -471,7 +482,8 @@ struct Phases {
     // coalesced write of each digit run
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < (FULL ? (uint32_t)TILE : cnt); i += SC_NT) {
-      const K k = sk[i];
+      const uint32_t src = PERM ? (uint32_t)perm[i] : i;
+      const K k = sk[src];
       const uint32_t o = (uint32_t)s_dst[digit_of(k, dg)] + i;  // < 2^30: unsigned math
 #ifdef DFR_DEBUG
       if (o < s.start || o >= s.start + s.len) {
@@ -480,7 +492,7 @@ struct Phases {
       }
 #endif
       dst[o] = k;
-      if (PAIRS) dstv[o] = sv[i];
+      if (PAIRS) dstv[o] = sv[src];
     }
   }
 
@@ -535,7 +547,8 @@ struct Phases {
   // tile's write-out, and tickets are still claimed in (nearly) completion
   // order, which keeps the look-back of later tiles short.
   // FUSEH: the middle pass of a fused level 0 also counts the joint histogram
-  template <int SC_NT, bool FUSEH = false>
+  // PERM (deal_tile): one tile buffer, refilled once the write-out is done
+  template <int SC_NT, bool FUSEH = false, bool PERM = false>
   static __device__ void scatter(const Params<K>& P, int j, uint32_t* sm) {
     constexpr int SC_W = SC_NT / 32;
     Ctl* c = P.ctl;
@@ -548,8 +561,10 @@ struct Phases {
     uint32_t* s_warp = reinterpret_cast<uint32_t*>(s_dst + 256);  // 16
     uint32_t* ti = s_warp + 16;                                   // 2 x 4 words
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(ti + 8);  // 2, 8-aligned
-    K* const kb0 = reinterpret_cast<K*>(sm + SCATTER_HDR_WORDS);  // 2 x TILE keys
-    V* const vb0 = reinterpret_cast<V*>(kb0 + 2 * TILE);          // 2 x TILE values
+    uint16_t* const perm = reinterpret_cast<uint16_t*>(sm + SCATTER_HDR_WORDS);  // PERM: TILE
+    K* const kb0 = PERM ? reinterpret_cast<K*>(perm + TILE)
+                        : reinterpret_cast<K*>(sm + SCATTER_HDR_WORDS);  // (1 or 2) x TILE keys
+    V* const vb0 = reinterpret_cast<V*>(kb0 + (PERM ? 1 : 2) * TILE);   // (1 or 2) x TILE values
     uint32_t* status = P.status + (size_t)j * P.status_stride;
     if (threadIdx.x == 0) {
       mbar_init(&bar[0], 1);
@@ -564,7 +579,7 @@ struct Phases {
     Seg s;
 
     for (int it = 0;; ++it) {
-      const int cb = it & 1;
+      const int cb = PERM ? 0 : (it & 1);
       for (int e = threadIdx.x; e < (SC_W + 1) * 256; e += SC_NT) whist[e] = 0;
       __syncthreads();  // ti[cb] visible; whist zeroed; the other buffer is free
       const uint32_t t = ti[cb * 4 + 0];
@@ -579,13 +594,17 @@ struct Phases {
       const bool tma = ti[cb * 4 + 2] != 0;
       K* sk = kb0 + cb * TILE;
       V* sv = vb0 + cb * TILE;
-      auto hook = [&]() {
-        if (threadIdx.x == 0)
-          claim_tile(P, j, q, nseg, total, ti + (cb ^ 1) * 4, kb0 + (cb ^ 1) * TILE,
-                     vb0 + (cb ^ 1) * TILE, &bar[cb ^ 1]);
+      auto claim_next = [&]() {
+        if (threadIdx.x == 0) {
+          const int nb = PERM ? 0 : (cb ^ 1);
+          claim_tile(P, j, q, nseg, total, ti + nb * 4, kb0 + nb * TILE, vb0 + nb * TILE, &bar[nb]);
+        }
+      };
+      auto hook = [&]() {  // double buffer: claim the next tile once the prefix is known
+        if (!PERM) claim_next();
       };
       if (!pass_active(s, j)) {
-        hook();
+        claim_next();
         continue;
       }
       const uint32_t lt = t - s.tile0;
@@ -607,11 +626,15 @@ struct Phases {
         __syncthreads();
       }
       if (cnt == (uint32_t)TILE)
-        deal_tile<SC_NT, true, FUSEH>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist, s_dst,
-                                      s_warp, dst, dstv, bstart);
+        deal_tile<SC_NT, true, FUSEH, PERM>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist,
+                                            s_dst, s_warp, dst, dstv, bstart, perm);
       else
-        deal_tile<SC_NT, false, FUSEH>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist, s_dst,
-                                       s_warp, dst, dstv, bstart);
+        deal_tile<SC_NT, false, FUSEH, PERM>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist,
+                                             s_dst, s_warp, dst, dstv, bstart, perm);
+      if (PERM) {  // single buffer: refill it once every thread is done with the write-out
+        __syncthreads();
+        claim_next();
+      }
       fence_proxy_async();  // generic smem accesses before a later TMA into this buffer
     }
     // every claimed ticket < total was processed, so no bulk copy is in flight here
