@@ -43,7 +43,7 @@ struct Phases {
   static constexpr size_t SMEM_SCATTER_P =
       SCATTER_HDR_WORDS * 4 + TILE * 2 + TILE * sizeof(K) + (PAIRS ? TILE * 4 : 0);
   // 2 windows (+ values) | fp16 composites | order | bitmask, misc, mbarriers
-  static constexpr size_t SMEM_DIVERT = 2 * (WIN * sizeof(K) + (PAIRS ? WIN * 4 : 0)) +
+  static constexpr size_t SMEM_DIVERT = 1 * (WIN * sizeof(K) + (PAIRS ? WIN * 4 : 0)) +
                                         (4 * WIN + 64) * 2 + WIN * 2 + (WIN / 32 + 12) * 4 + 16 + 16;
   static constexpr size_t SMEM_MID = 2 * MID_CAP * sizeof(K) + (PAIRS ? 2 * MID_CAP * 4 : 0) +
                                      (MID_CAP + 8) * sizeof(CT) + 3 * WARPS * 256 * 4 + 256 * 4 +
@@ -914,14 +914,13 @@ struct Phases {
     const uint32_t bm_a = smem_u32(S.bm);  // word index = position / 32 (zero words beyond both ends)
     const K pmask = (K)(~K(0) << shift);  // the group prefix bits of a key
     // ---- A: keys, bucket-start words
-    K key[DKPT];
-    uint32_t bw[DKPT];
+    uint32_t bw[DKPT];  // (keys are re-read in B: registers buy occupancy here)
 #pragma unroll
     for (int m = 0; m < DKPT; ++m) {
       const int i = wbase + 32 * m + lane;
-      key[m] = ldsk<K>(sk_a + KB * i);
+      const K km = ldsk<K>(sk_a + KB * i);
       const K kp = ldsk<K>(sk_a + KB * (i > 0 ? i - 1 : 0));
-      bool st = ((key[m] ^ kp) & pmask) != K(0);
+      bool st = ((km ^ kp) & pmask) != K(0);
       if (m == 0) st |= i == 0;
       if (EDGE) {
         const int r = r0 + i;
@@ -978,7 +977,7 @@ struct Phases {
         info[m] = DV_NONE;
         if (own && small) {
           info[m] = (uint32_t)bs | ((uint32_t)(be - bs) << 12);
-          const uint32_t c16 = comp.template get<LOSSY>(key[m], (uint32_t)(i - bs));
+          const uint32_t c16 = comp.template get<LOSSY>(ldsk<K>(sk_a + KB * i), (uint32_t)(i - bs));
           mev[m >> 1] |= c16 << (16 * (m & 1));
           sts16(cmp_a + 2 * (3 * bs + i), c16);
         }
@@ -1000,7 +999,7 @@ struct Phases {
         info[m] = DV_NONE;
         if (own && small) {
           info[m] = (uint32_t)bs | ((uint32_t)(be - bs) << 12);
-          const uint32_t c16 = comp.template get<LOSSY>(key[m], (uint32_t)(i - bs));
+          const uint32_t c16 = comp.template get<LOSSY>(ldsk<K>(sk_a + KB * i), (uint32_t)(i - bs));
           mev[m >> 1] |= c16 << (16 * (m & 1));
           sts16(cmp_a + 2 * (3 * bs + i), c16);
         }
@@ -1082,8 +1081,8 @@ struct Phases {
     DivertSmem S;
     char* base = reinterpret_cast<char*>(sm);
     S.win[0] = base;
-    S.win[1] = base + DV_WIN_BYTES;
-    S.cmp = reinterpret_cast<uint16_t*>(base + 2 * DV_WIN_BYTES);
+    S.win[1] = base;  // one window buffer: 10 CTAs/SM hide its refill
+    S.cmp = reinterpret_cast<uint16_t*>(base + DV_WIN_BYTES);
     S.order = S.cmp + DV_CMP;
     uint32_t* bm0 = reinterpret_cast<uint32_t*>(S.order + WIN);
     S.bm = bm0 + 4;
@@ -1105,7 +1104,7 @@ struct Phases {
     uint32_t cur_si = ~0u;  // the segment record and composite plan change rarely
     Seg s;
     Compo comp;
-    for (uint32_t ch = blockIdx.x; ch < total; ch += gridDim.x, b ^= 1) {
+    for (uint32_t ch = blockIdx.x; ch < total; ch += gridDim.x) {
       const uint32_t si = S.misc[2 * b];
       if (si != cur_si) {
         cur_si = si;
@@ -1113,9 +1112,6 @@ struct Phases {
         comp.init(8 * s.low, (int)P.n_d);
       }
       const bool tma = S.misc[2 * b + 1] != 0;
-      // the next window goes to the other buffer, free since the previous
-      // window's closing barrier: its load overlaps this whole window
-      if (threadIdx.x == 0) divert_prefetch(P, q, nseg, total, ch + gridDim.x, S, b ^ 1);
       int c0, r0, off;
       window_of(P, s, ch, c0, r0, off);
       if (s.flags & (SEG_DONE | SEG_SKIP_DIVERT | SEG_COPY)) {
@@ -1126,6 +1122,8 @@ struct Phases {
             if (PAIRS) P.Av[s.start + r] = P.Bv[s.start + r];
           }
         }
+        __syncthreads();
+        if (threadIdx.x == 0) divert_prefetch(P, q, nseg, total, ch + gridDim.x, S, 0);
         __syncthreads();
         continue;
       }
@@ -1156,6 +1154,8 @@ struct Phases {
         else      divert_window<NT, true, false>(P, s, S, sk_a, sv_a, r0, off, comp);
       }
       __syncthreads();  // window buffer, composites and order free
+      if (threadIdx.x == 0) divert_prefetch(P, q, nseg, total, ch + gridDim.x, S, 0);
+      __syncthreads();  // the next window's segment / tma flag visible
     }
   }
 
