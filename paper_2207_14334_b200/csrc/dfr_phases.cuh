@@ -418,12 +418,36 @@ struct Phases {
       run = tcount[dd];
       st_relaxed(status + (size_t)t * 256 + dd, (lt == 0 ? FLAG_INC : FLAG_AGG) | run);
     }
+    if (w == 0) {  // tile offsets of the 256 digits (8 per lane) into s_dst, free until the look-back
+      const uint4 c0 = *reinterpret_cast<const uint4*>(tcount + 8 * lane);
+      const uint4 c1 = *reinterpret_cast<const uint4*>(tcount + 8 * lane + 4);
+      const uint32_t c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      uint32_t sum = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum += c[k];
+      uint32_t x = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      uint32_t e0 = x - sum;
+      uint32_t ex[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        ex[k] = e0;
+        e0 += c[k];
+      }
+      *reinterpret_cast<uint4*>(s_dst + 8 * lane) = make_uint4(ex[0], ex[1], ex[2], ex[3]);
+      *reinterpret_cast<uint4*>(s_dst + 8 * lane + 4) = make_uint4(ex[4], ex[5], ex[6], ex[7]);
+    }
     warp_rank<SC_KPT, FULL>(dr, mywh);
-    uint32_t tot;
-    const uint32_t lstart = block_excl_scan<SC_NT>(run, s_warp, &tot);  // syncs: ranks done
+    __syncthreads();  // ranks and tile offsets done
     // per digit: warp bases in the tile = tile offset of the digit + counts of
     // the digit in earlier warps
+    uint32_t lstart = 0;
     if (dig_thread) {
+      lstart = (uint32_t)s_dst[dd];
       uint32_t acc = lstart;
 #pragma unroll
       for (int e = 0; e < SC_W; ++e) {
