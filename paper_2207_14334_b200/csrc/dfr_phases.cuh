@@ -529,6 +529,9 @@ struct Phases {
   // earlier tiles and writes every digit run contiguously.
   // thread 0: claim a ticket into ti[0..2] (ticket, segment, tma) and, for a
   // full aligned tile of an active segment, start its TMA bulk load
+  // (DEFER: ticket, segment and eligibility only; issue_tile starts the copy
+  // later — ti is then final before the caller's next barrier)
+  template <bool DEFER = false>
   static __device__ __forceinline__ void claim_tile(const Params<K>& P, int j, const Seg* q,
                                                     uint32_t nseg, uint32_t total, uint32_t* ti,
                                                     K* kb, V* vb, unsigned long long* bar) {
@@ -546,6 +549,19 @@ struct Phases {
     const V* srcv = PAIRS ? (sb ? P.Bv : P.Av) + s.start + lt * TILE : nullptr;
     if ((reinterpret_cast<uintptr_t>(src) & 15) || (PAIRS && (reinterpret_cast<uintptr_t>(srcv) & 15)))
       return;
+    ti[2] = 1;
+    if (!DEFER) issue_tile(P, j, q, ti, kb, vb, bar);
+  }
+  // thread 0: start the TMA bulk copy of the claimed tile in ti (ti[2] = 1)
+  static __device__ __forceinline__ void issue_tile(const Params<K>& P, int j, const Seg* q,
+                                                    const uint32_t* ti, K* kb, V* vb,
+                                                    unsigned long long* bar) {
+    if (!ti[2]) return;
+    const Seg& s = q[ti[1]];
+    const uint32_t lt = ti[0] - s.tile0;
+    const uint32_t sb = src_buf(s, j);
+    const K* src = (sb ? P.B : P.A) + s.start + lt * TILE;
+    const V* srcv = PAIRS ? (sb ? P.Bv : P.Av) + s.start + lt * TILE : nullptr;
     fence_proxy_async();
     const uint32_t bytes = TILE * sizeof(K) + (PAIRS ? TILE * 4 : 0);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
@@ -562,7 +578,6 @@ struct Phases {
               smem_u32(vb)),
           "l"(srcv), "r"((uint32_t)(TILE * 4)), "r"(smem_u32(bar))
           : "memory");
-    ti[2] = 1;
   }
 
   // Persistent CTA with two tile buffers.  The next tile's ticket is claimed,
@@ -602,10 +617,17 @@ struct Phases {
     uint32_t cur_si = ~0u, bstart = 0;
     Seg s;
 
+    if (PERM) {
+      for (int e = threadIdx.x; e < (SC_W + 1) * 256; e += SC_NT) whist[e] = 0;
+    }
     for (int it = 0;; ++it) {
       const int cb = PERM ? 0 : (it & 1);
-      for (int e = threadIdx.x; e < (SC_W + 1) * 256; e += SC_NT) whist[e] = 0;
-      __syncthreads();  // ti[cb] visible; whist zeroed; the other buffer is free
+      if (!PERM) {
+        for (int e = threadIdx.x; e < (SC_W + 1) * 256; e += SC_NT) whist[e] = 0;
+      }
+      // PERM: the previous tile's closing barrier already made ti visible and
+      // the zeroed counters; the first tile needs this one
+      if (!PERM || it == 0) __syncthreads();  // ti[cb] visible; whist zeroed; other buffer free
       const uint32_t t = ti[cb * 4 + 0];
       if (t >= total) break;
       const uint32_t si = ti[cb * 4 + 1];
@@ -624,11 +646,17 @@ struct Phases {
           claim_tile(P, j, q, nseg, total, ti + nb * 4, kb0 + nb * TILE, vb0 + nb * TILE, &bar[nb]);
         }
       };
-      auto hook = [&]() {  // double buffer: claim the next tile once the prefix is known
-        if (!PERM) claim_next();
+      // claim the next tile once this one's prefix is known (tickets in
+      // completion order); PERM: its copy starts after the write-out
+      auto hook = [&]() {
+        if (!PERM)
+          claim_next();
+        else if (threadIdx.x == 0)
+          claim_tile<true>(P, j, q, nseg, total, ti, kb0, vb0, &bar[0]);
       };
       if (!pass_active(s, j)) {
         claim_next();
+        if (PERM) __syncthreads();
         continue;
       }
       const uint32_t lt = t - s.tile0;
@@ -656,8 +684,12 @@ struct Phases {
         deal_tile<SC_NT, false, FUSEH, PERM>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist,
                                              s_dst, s_warp, dst, dstv, bstart, perm);
       if (PERM) {  // single buffer: refill it once every thread is done with the write-out
+        for (int e = threadIdx.x; e < (SC_W + 1) * 256; e += SC_NT) whist[e] = 0;
         __syncthreads();
-        claim_next();
+        if (threadIdx.x == 0) {
+          fence_proxy_async();
+          issue_tile(P, j, q, ti, kb0, vb0, &bar[0]);
+        }
       }
       fence_proxy_async();  // generic smem accesses before a later TMA into this buffer
     }
