@@ -18,6 +18,9 @@ namespace dfr {
 
 constexpr int THREADS = 256;             // one CTA = 8 warps
 constexpr int WARPS = THREADS / 32;
+#ifndef DFR_LB_SLEEP
+#define DFR_LB_SLEEP 64
+#endif
 constexpr int KPT = 16;                  // keys per thread per tile
 constexpr int TILE = THREADS * KPT;      // 4096 keys per tile (hist / deal)
 constexpr int WIN = 1024;                // diversion window (keys) per CTA

@@ -196,13 +196,32 @@ struct Phases {
         if (cp)
 #pragma unroll
           for (int u = 0; u < U; ++u) reinterpret_cast<uint4*>(cp)[vb + u * THREADS + threadIdx.x] = x[u];
+        // one warp vote per block: do all U*VEC*32 keys share lane 0's group
+        // prefix?  OR of (k ^ k0) | (k0 ^ kref) over the segment equals the
+        // OR of (k ^ kref), so the diff mask comes from the same accumulator
+        const K k0 = __shfl_sync(0xffffffffu, reinterpret_cast<const K*>(&x[0])[0], 0);
+        K acc = 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const K* kk = reinterpret_cast<const K*>(&x[u]);
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            diff |= (unsigned long long)(kk[e] ^ kref);
-            count_key<NP>(shw, kk[e], true, low);
+          for (int e = 0; e < VEC; ++e) acc |= kk[e] ^ k0;
+        }
+        diff |= (unsigned long long)(acc | (k0 ^ kref));
+        if (__all_sync(0xffffffffu, (acc >> (8 * low)) == K(0))) {
+          if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+            for (int j = 0; j < NP; ++j)
+              red_add_shared(shw + 4 * (j * 256 + digit_of(k0, low + j)), 32u * U * VEC);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const K* kk = reinterpret_cast<const K*>(&x[u]);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e)
+#pragma unroll
+              for (int j = 0; j < NP; ++j) red_add_shared(shw + 4 * (j * 256 + digit_of(kk[e], low + j)), 1u);
           }
         }
       }
@@ -494,6 +513,7 @@ struct Phases {
             }
           }
           if (done) break;
+          if (k == 0) __nanosleep(DFR_LB_SLEEP);  // predecessor not published: yield the issue slots
           tt -= k;
         }
         st_relaxed(status + (size_t)t * 256 + dd, FLAG_INC | (excl + run));
