@@ -18,9 +18,20 @@ namespace dfr {
 
 constexpr int THREADS = 256;             // one CTA = 8 warps
 constexpr int WARPS = THREADS / 32;
+// tuning knobs (tools/variants.sh builds alternatives side by side)
 #ifndef DFR_LB_SLEEP
-#define DFR_LB_SLEEP 64
+#define DFR_LB_SLEEP 64  // ns of back-off when a look-back round makes no progress
 #endif
+#ifndef DFR_LB
+#define DFR_LB 8  // look-back predecessors loaded per round trip
+#endif
+#ifndef DFR_WO_UNROLL
+#define DFR_WO_UNROLL 4  // deal write-out unroll
+#endif
+#ifndef DFR_DV_CU
+#define DFR_DV_CU 2  // diversion rank-count loop unroll
+#endif
+constexpr int WO_UNROLL = DFR_WO_UNROLL, DV_CU = DFR_DV_CU;
 constexpr int KPT = 16;                  // keys per thread per tile
 constexpr int TILE = THREADS * KPT;      // 4096 keys per tile (hist / deal)
 constexpr int WIN = 1024;                // diversion window (keys) per CTA
@@ -269,8 +280,42 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
 // out = digit | rank << 16.
 template <bool FULL>
 __device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
-  // digit bit b moved to the sign position: its ballot, xor the spread of
-  // the lane's own bit, marks the lanes that differ in that bit
+  // lanes whose digit equals this lane's: AND over the digit bits of the
+  // bit's ballot, complemented where this lane's bit is 0
+#ifdef DFR_EXPERIMENT_NOPEERS
+  if (FULL) return 1u << (threadIdx.x & 31);  // timing experiment only: wrong output
+#endif
+#ifndef DFR_PEERS_C
+  // per bit: lop3 -> predicate, vote, predicated not, and (4 SASS instructions)
+  uint32_t peers;
+  if (FULL)
+    asm("{\n .reg .pred p;\n .reg .b32 v, t;\n"
+        " and.b32 t, %1, 1; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; mov.b32 %0, v;\n"
+        " and.b32 t, %1, 2; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        " and.b32 t, %1, 4; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        " and.b32 t, %1, 8; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        " and.b32 t, %1, 16; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        " and.b32 t, %1, 32; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        " and.b32 t, %1, 64; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        " and.b32 t, %1, 128; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        "}" : "=r"(peers) : "r"(d));
+  else  // digit 256 marks an empty slot: a ninth bit
+    asm("{\n .reg .pred p;\n .reg .b32 v, t;\n"
+        " and.b32 t, %1, 1; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; mov.b32 %0, v;\n"
+        " and.b32 t, %1, 2; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        " and.b32 t, %1, 4; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        " and.b32 t, %1, 8; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        " and.b32 t, %1, 16; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        " and.b32 t, %1, 32; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        " and.b32 t, %1, 64; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        " and.b32 t, %1, 128; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        " and.b32 t, %1, 256; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
+        "}" : "=r"(peers) : "r"(d));
+  return peers;
+#endif
+  // C form (-DDFR_PEERS_C; 5 instructions per bit): the bit moved to the sign
+  // position, its ballot xor the spread of the lane's own bit marks the lanes
+  // that differ in that bit
   constexpr int NB = FULL ? 8 : 9;
   const int x = (int)(d << (32 - NB));
   uint32_t diff = 0;

@@ -492,11 +492,15 @@ struct Phases {
     }
     if (dig_thread) {
       uint32_t excl = 0;
+#ifdef DFR_EXPERIMENT_NOLB
+      if (false) {  // timing experiment only: wrong output
+#else
       if (lt > 0) {  // decoupled look-back, up to LB predecessors per round trip
+#endif
         int tt = (int)t - 1;
         const int t0 = (int)s.tile0;  // publishes FLAG_INC, so the walk ends there
         while (true) {
-          constexpr int LB = 8;  // predecessors per look-back round trip
+          constexpr int LB = DFR_LB;  // predecessors per look-back round trip
           uint32_t v[LB];
 #pragma unroll
           for (int k = 0; k < LB; ++k)
@@ -524,7 +528,7 @@ struct Phases {
     after_lookback();  // thread 0: claim the next tile, start its TMA load
     __syncthreads();
     // coalesced write of each digit run
-#pragma unroll 4
+#pragma unroll WO_UNROLL
     for (uint32_t i = threadIdx.x; i < (FULL ? (uint32_t)TILE : cnt); i += SC_NT) {
       const uint32_t src = PERM ? (uint32_t)perm[i] : i;
       const K k = sk[src];
@@ -1102,7 +1106,7 @@ struct Phases {
       uint32_t pa = cmp_a + 8 * bs;
       const uint32_t pe = pa + 8 * ng;
       __half2 acc = __float2half2_rn(0.f);
-#pragma unroll 2
+#pragma unroll DV_CU
       for (; pa < pe; pa += 8) {
         const uint2 v = lds64v(pa);
         acc = __hadd2(acc, __hlt2(*reinterpret_cast<const __half2*>(&v.x), me2));
