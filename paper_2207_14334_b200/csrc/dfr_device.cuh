@@ -22,6 +22,9 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_LB_SLEEP
 #define DFR_LB_SLEEP 64  // ns of back-off when a look-back round makes no progress
 #endif
+#ifndef DFR_RANK_G
+#define DFR_RANK_G 4  // keys whose peer masks are computed together in warp_rank
+#endif
 #ifndef DFR_LB
 #define DFR_LB 8  // look-back predecessors loaded per round trip
 #endif
@@ -299,6 +302,7 @@ __device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
         " and.b32 t, %1, 64; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
         " and.b32 t, %1, 128; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
         "}" : "=r"(peers) : "r"(d));
+#ifndef DFR_PEERS_C9
   else  // digit 256 marks an empty slot: a ninth bit
     asm("{\n .reg .pred p;\n .reg .b32 v, t;\n"
         " and.b32 t, %1, 1; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; mov.b32 %0, v;\n"
@@ -312,6 +316,9 @@ __device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
         " and.b32 t, %1, 256; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
         "}" : "=r"(peers) : "r"(d));
   return peers;
+#else
+  if (FULL) return peers;
+#endif
 #endif
   // C form (-DDFR_PEERS_C; 5 instructions per bit): the bit moved to the sign
   // position, its ballot xor the spread of the lane's own bit marks the lanes
@@ -328,13 +335,13 @@ __device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
   return ~diff;
 }
 
-template <int N, bool FULL>
+template <int N, bool FULL, bool LDS = false>
 __device__ __forceinline__ void warp_rank(uint32_t (&io)[N], uint32_t* whist) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
   // peer masks of G items first (independent ballot chains), then their
   // counter updates in item order
-  constexpr int G = 4;
+  constexpr int G = DFR_RANK_G;
   static_assert(N % G == 0, "items per group");
 #pragma unroll
   for (int j0 = 0; j0 < N; j0 += G) {
@@ -344,10 +351,18 @@ __device__ __forceinline__ void warp_rank(uint32_t (&io)[N], uint32_t* whist) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint32_t d = io[j0 + g];
-      const uint32_t leader = __ffs(peers[g]) - 1;
       uint32_t old = 0;
-      if (lane == leader && (FULL || d < 256)) old = atomicAdd(&whist[d], __popc(peers[g]));
-      old = __shfl_sync(0xffffffffu, old, leader);
+      if (LDS) {
+        // every lane reads the counter, the last peer lane writes it back (a
+        // warp's shared-memory accesses are performed in instruction order)
+        const bool ok = FULL || d < 256;
+        old = ok ? whist[d] : 0u;
+        if (ok && lane == 31 - __clz(peers[g])) whist[d] = old + __popc(peers[g]);
+      } else {
+        const uint32_t leader = __ffs(peers[g]) - 1;
+        if (lane == leader && (FULL || d < 256)) old = atomicAdd(&whist[d], __popc(peers[g]));
+        old = __shfl_sync(0xffffffffu, old, leader);
+      }
       io[j0 + g] = d | ((old + __popc(peers[g] & lt)) << 16);
     }
   }

@@ -460,7 +460,7 @@ struct Phases {
       *reinterpret_cast<uint4*>(s_dst + 8 * lane) = make_uint4(ex[0], ex[1], ex[2], ex[3]);
       *reinterpret_cast<uint4*>(s_dst + 8 * lane + 4) = make_uint4(ex[4], ex[5], ex[6], ex[7]);
     }
-    warp_rank<SC_KPT, FULL>(dr, mywh);
+    warp_rank<SC_KPT, FULL, PERM>(dr, mywh);
     __syncthreads();  // ranks and tile offsets done
     // per digit: warp bases in the tile = tile offset of the digit + counts of
     // the digit in earlier warps
