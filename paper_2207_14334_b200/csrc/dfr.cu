@@ -289,7 +289,8 @@ static Layout make_layout(size_t n, int kb, int vb, uint32_t n_d, int min_passes
   L.hist = take(L.hist_rows * 256 * 4);
   int passes = est_top_passes(n, n_d);  // no group of any level has more passes
   passes = passes < min_passes ? min_passes : (passes > MAX_PASSES ? MAX_PASSES : passes);
-  L.status = take((size_t)passes * L.tiles_max * 256 * 4);
+  // LB_PAD rows in front: the look-back loads up to DFR_LB rows below tile 0
+  L.status = take(((size_t)passes * L.tiles_max + LB_PAD) * 256 * 4);
   L.fh = fuse ? take(65536 * 4) : 0;      // joint histogram of the two low group digits
   L.ftiles = fuse ? take(65536 * 8) : 0;  // run-aligned tiles of the fused pass
   L.total = off;
@@ -310,7 +311,7 @@ static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals,
   P.segq[1] = reinterpret_cast<Seg*>(ws + L.segq1);
   P.midq = reinterpret_cast<MidE*>(ws + L.midq);
   P.hist = reinterpret_cast<uint32_t*>(ws + L.hist);
-  P.status = reinterpret_cast<uint32_t*>(ws + L.status);
+  P.status = reinterpret_cast<uint32_t*>(ws + L.status) + LB_PAD * 256;
   P.status_stride = L.tiles_max * 256;
   P.H = L.fh ? reinterpret_cast<uint32_t*>(ws + L.fh) : nullptr;
   P.ftiles = L.ftiles ? reinterpret_cast<uint2*>(ws + L.ftiles) : nullptr;

@@ -34,6 +34,8 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_DV_CU
 #define DFR_DV_CU 2  // diversion rank-count loop unroll
 #endif
+constexpr int LB_PAD = 16;  // status rows in front of pass 0's table (>= DFR_LB)
+static_assert(DFR_LB <= LB_PAD, "look-back pad");
 constexpr int WO_UNROLL = DFR_WO_UNROLL, DV_CU = DFR_DV_CU;
 constexpr int KPT = 16;                  // keys per thread per tile
 constexpr int TILE = THREADS * KPT;      // 4096 keys per tile (hist / deal)
@@ -136,6 +138,20 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+// ld_relaxed at p + OFF bytes (immediate offset: no address arithmetic)
+template <int OFF>
+__device__ __forceinline__ uint32_t ld_relaxed_off(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1+%2];" : "=r"(v) : "l"(p), "n"(OFF) : "memory");
+  return v;
+}
+template <int LB, int K = 0>
+__device__ __forceinline__ void ld_lookback(const uint32_t* p, uint32_t (&v)[LB]) {
+  if constexpr (K < LB) {
+    v[K] = ld_relaxed_off<-1024 * K>(p);
+    ld_lookback<LB, K + 1>(p, v);
+  }
 }
 __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

@@ -498,13 +498,14 @@ struct Phases {
       if (lt > 0) {  // decoupled look-back, up to LB predecessors per round trip
 #endif
         int tt = (int)t - 1;
-        const int t0 = (int)s.tile0;  // publishes FLAG_INC, so the walk ends there
         while (true) {
           constexpr int LB = DFR_LB;  // predecessors per look-back round trip
+          // LB predecessors tt, tt-1, ... in one round trip; rows before the
+          // segment's first tile t0 may be read (status has LB pad rows in
+          // front) but are never used: t0 publishes FLAG_INC, and the walk
+          // stops at the first FLAG_INC or unpublished entry
           uint32_t v[LB];
-#pragma unroll
-          for (int k = 0; k < LB; ++k)
-            v[k] = (tt - k >= t0) ? ld_relaxed(status + (size_t)(tt - k) * 256 + dd) : FLAG_INC;
+          ld_lookback<LB>(status + (size_t)tt * 256 + dd, v);
           int k = 0;
           bool done = false;
 #pragma unroll
