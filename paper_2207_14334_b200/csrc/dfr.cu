@@ -84,6 +84,25 @@ __global__ void __launch_bounds__(THREADS) k_plan2(const __grid_constant__ Param
   Phases<K, PAIRS>::plan2(P, sm);
 }
 
+// Plan of recursion level 1 (the queue the level-0 diversion filled), run by
+// the stand-alone kernels at full occupancy; an empty queue leaves an empty
+// level, on which they return at once.
+template <class K, bool PAIRS>
+__global__ void __launch_bounds__(THREADS) k_lplan(const __grid_constant__ Params<K> P) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  Ctl* c = P.ctl;
+  if (*(volatile uint32_t*)&c->next_count == 0) {
+    if (threadIdx.x == 0) {
+      c->nseg = 0;
+      c->total_tiles = 0;
+      c->total_chunks = 0;
+      c->max_p = 0;
+    }
+    return;
+  }
+  Phases<K, PAIRS>::plan(P, sm);
+}
+
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(Phases<K, PAIRS>::SC_NT, 4) k_scatter(const __grid_constant__ Params<K> P, int j) {
   extern __shared__ __align__(16) uint32_t sm[];
@@ -418,6 +437,15 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
     k_divert<K, PAIRS><<<g_dv, Ph::DV_NT, Ph::SMEM_DIVERT, st>>>(P);
     pe.end(DFR_PHASE_DIVERT);
     pe.begin(DFR_PHASE_LEVELS);
+    // level 1 through the stand-alone kernels (large recursions: c3, c4,
+    // c5-low20 put most of their keys there), levels 2.. in k_levels
+    k_lplan<K, PAIRS><<<1, THREADS, 64, st>>>(P);
+    k_hist<K, PAIRS><<<g_hist, THREADS, Ph::SMEM_HIST, st>>>(P);
+    k_plan2<K, PAIRS><<<4 * sms, THREADS, 64, st>>>(P);  // one block per segment
+    for (int j = 0; j < MAX_PASSES; ++j)
+      k_scatter<K, PAIRS><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER_P, st>>>(P, j);
+    k_divert<K, PAIRS><<<g_dv, Ph::DV_NT, Ph::SMEM_DIVERT, st>>>(P);
+    g_launches += 4 + MAX_PASSES;
     void* args[] = {&P};
     const int g_lv = sms * std::max(1, dv.occ_levels);
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_levels<K, PAIRS>, g_lv, THREADS,

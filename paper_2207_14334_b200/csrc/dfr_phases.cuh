@@ -1597,6 +1597,14 @@ struct Phases {
       const int len = me.len;
       const K* X = me.buf ? P.B : P.A;
       const V* Xv = me.buf ? P.Bv : P.Av;
+      if (me.hi < 0) {  // digits exhausted: a constant bucket, sorted (Alg. 2 l.17-18)
+        if (me.buf)  // left in the scratch buffer: copy out
+          for (int i = threadIdx.x; i < len; i += THREADS) {
+            P.A[me.start + i] = P.B[me.start + i];
+            if (PAIRS) P.Av[me.start + i] = P.Bv[me.start + i];
+          }
+        continue;
+      }
       for (int i = threadIdx.x; i < len; i += THREADS) {
         S0[i] = X[me.start + i];
         if (PAIRS) V0[i] = Xv[me.start + i];
