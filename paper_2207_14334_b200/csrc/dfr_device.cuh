@@ -51,6 +51,7 @@ constexpr uint32_t VAL_MASK = (1u << 30) - 1;
 constexpr uint32_t SEG_SKIP_DIVERT = 1u << 8;  // no diversion scan this level
 constexpr uint32_t SEG_COPY = 1u << 9;         // finished, data in B: copy to A
 constexpr uint32_t SEG_DONE = 1u << 10;        // finished in A
+constexpr uint32_t SEG_SORTED = 1u << 11;      // passes reach digit 0: sorted after them
 
 struct Seg {                    // one DFR invocation on a contiguous bucket
   uint32_t start, len;          // element range in the arrays

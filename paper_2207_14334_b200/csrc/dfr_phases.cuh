@@ -356,6 +356,10 @@ struct Phases {
           }
         }
       }
+      // recursion levels: when the passes end on digit 0 every bucket of the
+      // scan (Alg. 4 l.8) is a constant key -- insertion sort and recursion
+      // leave it as it is -- so the diversion only moves the segment to A
+      if (executed > 0 && s.low == 0 && c->level > 0) flags |= SEG_SORTED;
       if (threadIdx.x == 0) {
         q[si].flags = flags;
         q[si].final_buf = s.buf ^ (executed & 1u);
@@ -877,7 +881,7 @@ struct Phases {
     const uint32_t si = upper_index(nseg, ch, [&](uint32_t i) { return q[i].chunk0; });
     S.misc[2 * b] = si;
     const Seg& s = q[si];
-    if (s.flags & (SEG_DONE | SEG_SKIP_DIVERT | SEG_COPY)) return;
+    if (s.flags & (SEG_DONE | SEG_SKIP_DIVERT | SEG_COPY | SEG_SORTED)) return;
     int c0, r0, off;
     window_of(P, s, ch, c0, r0, off);
     const long long abs0 = (long long)s.start + r0;
@@ -1195,8 +1199,9 @@ struct Phases {
       const bool tma = S.misc[2 * b + 1] != 0;
       int c0, r0, off;
       window_of(P, s, ch, c0, r0, off);
-      if (s.flags & (SEG_DONE | SEG_SKIP_DIVERT | SEG_COPY)) {
-        if (s.flags & SEG_COPY) {  // finished bucket left in B: copy out
+      if (s.flags & (SEG_DONE | SEG_SKIP_DIVERT | SEG_COPY | SEG_SORTED)) {
+        // finished bucket left in B: copy out
+        if ((s.flags & SEG_COPY) || ((s.flags & SEG_SORTED) && s.final_buf)) {
           const int c1 = min((int)s.len, c0 + (int)P.chunk);
           for (int r = c0 + threadIdx.x; r < c1; r += blockDim.x) {
             P.A[s.start + r] = P.B[s.start + r];
@@ -1269,7 +1274,7 @@ struct Phases {
     __shared__ uint32_t s_w[32], s_w2[32], s_m[32];
     const Seg s = P.segq[c->cur][0];
     const bool eligible = P.fuse && c->level == 0 && c->nseg == 1 && s.p == 3 &&
-                          (s.flags & (0xfu | SEG_SKIP_DIVERT | SEG_COPY | SEG_DONE)) == 0;
+                          (s.flags & (0xfu | SEG_SKIP_DIVERT | SEG_COPY | SEG_DONE | SEG_SORTED)) == 0;
     if (!eligible) {
       if (threadIdx.x == 0) c->fused_ok = 0;
       return;
