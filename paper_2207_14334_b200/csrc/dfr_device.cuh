@@ -385,6 +385,42 @@ __device__ __forceinline__ void warp_rank(uint32_t (&io)[N], uint32_t* whist) {
   }
 }
 
+// cooperative copy of n elements by nt threads (this one: tid): 16-byte
+// vectors when dst and src share their alignment, four accesses in flight
+template <class T>
+__device__ __forceinline__ void coop_copy(T* dst, const T* src, uint32_t n, uint32_t tid,
+                                          uint32_t nt) {
+  if ((((uintptr_t)dst ^ (uintptr_t)src) & 15) == 0) {
+    constexpr uint32_t E = 16 / sizeof(T);
+    uint32_t head = (uint32_t)(((16 - ((uintptr_t)src & 15)) & 15) / sizeof(T));
+    if (head > n) head = n;
+    const uint32_t nv = (n - head) / E;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+    uint32_t v = tid;
+    for (; v + 3 * nt < nv; v += 4 * nt) {
+      const uint4 x0 = s4[v], x1 = s4[v + nt], x2 = s4[v + 2 * nt], x3 = s4[v + 3 * nt];
+      d4[v] = x0;
+      d4[v + nt] = x1;
+      d4[v + 2 * nt] = x2;
+      d4[v + 3 * nt] = x3;
+    }
+    for (; v < nv; v += nt) d4[v] = s4[v];
+    for (uint32_t i = tid; i < head; i += nt) dst[i] = src[i];
+    for (uint32_t i = head + nv * E + tid; i < n; i += nt) dst[i] = src[i];
+  } else {
+    uint32_t i = tid;
+    for (; i + 3 * nt < n; i += 4 * nt) {
+      const T x0 = src[i], x1 = src[i + nt], x2 = src[i + 2 * nt], x3 = src[i + 3 * nt];
+      dst[i] = x0;
+      dst[i + nt] = x1;
+      dst[i + 2 * nt] = x2;
+      dst[i + 3 * nt] = x3;
+    }
+    for (; i < n; i += nt) dst[i] = src[i];
+  }
+}
+
 // binary search: largest i in [0, n) with key(i) <= t (key non-decreasing, key(0) = 0)
 template <class F>
 __device__ __forceinline__ uint32_t upper_index(uint32_t n, uint32_t t, F key) {

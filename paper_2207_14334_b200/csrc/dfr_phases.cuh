@@ -1203,10 +1203,20 @@ struct Phases {
         // finished bucket left in B: copy out
         if ((s.flags & SEG_COPY) || ((s.flags & SEG_SORTED) && s.final_buf)) {
           const int c1 = min((int)s.len, c0 + (int)P.chunk);
-          for (int r = c0 + threadIdx.x; r < c1; r += blockDim.x) {
-            P.A[s.start + r] = P.B[s.start + r];
-            if (PAIRS) P.Av[s.start + r] = P.Bv[s.start + r];
+          const int nt = blockDim.x;
+          int r = c0 + threadIdx.x;
+          K* dA = P.A + s.start;
+          const K* sB = P.B + s.start;
+          for (; r + 3 * nt < c1; r += 4 * nt) {  // four loads in flight
+            const K x0 = sB[r], x1 = sB[r + nt], x2 = sB[r + 2 * nt], x3 = sB[r + 3 * nt];
+            dA[r] = x0;
+            dA[r + nt] = x1;
+            dA[r + 2 * nt] = x2;
+            dA[r + 3 * nt] = x3;
           }
+          for (; r < c1; r += nt) dA[r] = sB[r];
+          if (PAIRS)
+            for (int rv = c0 + threadIdx.x; rv < c1; rv += nt) P.Av[s.start + rv] = P.Bv[s.start + rv];
         }
         __syncthreads();
         if (threadIdx.x == 0) divert_prefetch(P, q, nseg, total, ch + gridDim.x, S, 0);
@@ -1604,9 +1614,9 @@ struct Phases {
       const V* Xv = me.buf ? P.Bv : P.Av;
       if (me.hi < 0) {  // digits exhausted: a constant bucket, sorted (Alg. 2 l.17-18)
         if (me.buf)  // left in the scratch buffer: copy out
-          for (int i = threadIdx.x; i < len; i += THREADS) {
-            P.A[me.start + i] = P.B[me.start + i];
-            if (PAIRS) P.Av[me.start + i] = P.Bv[me.start + i];
+          {
+            coop_copy(P.A + me.start, P.B + me.start, (uint32_t)len, threadIdx.x, THREADS);
+            if (PAIRS) coop_copy(P.Av + me.start, P.Bv + me.start, (uint32_t)len, threadIdx.x, THREADS);
           }
         continue;
       }
