@@ -134,9 +134,15 @@ __global__ void __launch_bounds__(Phases<K, PAIRS>::FNT, 2) k_fused(const __grid
 }
 
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(THREADS, 2) k_mid(const __grid_constant__ Params<K> P) {
+__global__ void __launch_bounds__(THREADS, 2) k_mid(const __grid_constant__ Params<K> P, int len_lo) {
   extern __shared__ __align__(16) uint32_t sm[];
-  Phases<K, PAIRS>::mid(P, sm);
+  Phases<K, PAIRS>::template mid<MID_CAP>(P, sm, len_lo);
+}
+// the mid buckets of at most MID_CAP_S keys, at 4 CTAs/SM
+template <class K, bool PAIRS>
+__global__ void __launch_bounds__(THREADS, 4) k_mid_s(const __grid_constant__ Params<K> P) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  Phases<K, PAIRS>::template mid<MID_CAP_S>(P, sm, 0);
 }
 
 // Recursion levels 1.. (Alg. 4 l.11 applied to every queued large bucket at
@@ -212,7 +218,8 @@ struct PhaseEv {  // optional caller-provided events around each phase
 
 struct Dev {
   int sms = 0;
-  int occ_hist = 0, occ_scatter = 0, occ_divert = 0, occ_mid = 0, occ_levels = 0, occ_fused = 0;
+  int occ_hist = 0, occ_scatter = 0, occ_divert = 0, occ_mid = 0, occ_mid_s = 0, occ_levels = 0,
+      occ_fused = 0;
 };
 
 template <class K, bool PAIRS>
@@ -262,6 +269,7 @@ static cudaError_t get_dev(Dev& out) {
             &d.occ_divert, (const void*)k_divert<K, PAIRS>, Ph::DV_NT, Ph::SMEM_DIVERT);
     }
     setup((const void*)k_mid<K, PAIRS>, Ph::SMEM_MID, &d.occ_mid);
+    setup((const void*)k_mid_s<K, PAIRS>, Ph::SMEM_MID_S, &d.occ_mid_s);
     if (err == cudaSuccess) {  // fused last pass: FNT-thread CTAs
       err = cudaFuncSetAttribute((const void*)k_fused<K, PAIRS>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_FUSED);
@@ -399,7 +407,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
     for (int i = 0; i < DFR_PHASE_MID; ++i) pe.skip(i);
     pe.begin(DFR_PHASE_MID);
     k_seed_mid<K, PAIRS><<<1, 1, 0, st>>>(P, nn);
-    k_mid<K, PAIRS><<<1, THREADS, Ph::SMEM_MID, st>>>(P);
+    k_mid<K, PAIRS><<<1, THREADS, Ph::SMEM_MID, st>>>(P, 0);
     pe.end(DFR_PHASE_MID);
     g_launches += 2;
   } else {
@@ -457,9 +465,10 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
     }
     pe.begin(DFR_PHASE_MID);
     const int g_mid = sms * std::max(1, dv.occ_mid);
-    k_mid<K, PAIRS><<<g_mid, THREADS, Ph::SMEM_MID, st>>>(P);
+    k_mid_s<K, PAIRS><<<sms * std::max(1, dv.occ_mid_s), THREADS, Ph::SMEM_MID_S, st>>>(P);
+    k_mid<K, PAIRS><<<g_mid, THREADS, Ph::SMEM_MID, st>>>(P, MID_CAP_S);
     pe.end(DFR_PHASE_MID);
-    g_launches += 6 + p0;
+    g_launches += 7 + p0;
   }
   cudaError_t e = cudaGetLastError();
   int rc = (e == cudaSuccess) ? DFR_OK : DFR_ERR_CUDA;

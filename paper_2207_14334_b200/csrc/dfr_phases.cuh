@@ -45,9 +45,13 @@ struct Phases {
   // 2 windows (+ values) | fp16 composites | order | bitmask, misc, mbarriers
   static constexpr size_t SMEM_DIVERT = 1 * (WIN * sizeof(K) + (PAIRS ? WIN * 4 : 0)) +
                                         (4 * WIN + 64) * 2 + WIN * 2 + (WIN / 32 + 12) * 4 + 16 + 16;
-  static constexpr size_t SMEM_MID = 2 * MID_CAP * sizeof(K) + (PAIRS ? 2 * MID_CAP * 4 : 0) +
-                                     (MID_CAP + 8) * sizeof(CT) + 3 * WARPS * 256 * 4 + 256 * 4 +
-                                     (MID_CAP / 32 + 8) * 4 + 512 * 8 + 128;
+  template <int CAP>
+  static constexpr size_t smem_mid() {
+    return 2 * CAP * sizeof(K) + (PAIRS ? 2 * CAP * 4 : 0) + (CAP + 8) * sizeof(CT) +
+           3 * WARPS * 256 * 4 + 256 * 4 + (CAP / 32 + 8) * 4 + 512 * 8 + 128;
+  }
+  static constexpr size_t SMEM_MID = smem_mid<MID_CAP>();
+  static constexpr size_t SMEM_MID_S = smem_mid<MID_CAP_S>();
   static constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
   static constexpr size_t SMEM_LEVEL =
       cmax(cmax(SMEM_HIST, SMEM_SCATTER), cmax(SMEM_DIVERT, SMEM_MID));
@@ -1540,6 +1544,7 @@ struct Phases {
 
   // ------------------------------------------------------------------ mid
   // stable counting pass over smem range [lo, lo+L) on digit g: a -> b
+  template <int MK>  // keys per thread: L <= THREADS * MK
   static __device__ void smem_pass(const K* a, K* b, const V* av, V* bv, int lo, int L, int g,
                                    uint32_t* whist, uint32_t* wmask, uint32_t* s_lstart,
                                    uint32_t* s_warp) {
@@ -1547,18 +1552,18 @@ struct Phases {
 #pragma unroll
     for (int e = 0; e < WARPS; ++e) whist[e * 256 + threadIdx.x] = 0;
     __syncthreads();
-    K key[KPT];
-    V val[KPT];
-    uint32_t dr[KPT];
+    K key[MK];
+    V val[MK];
+    uint32_t dr[MK];
 #pragma unroll
-    for (int jj = 0; jj < KPT; ++jj) {
-      const int rel = w * 32 * KPT + jj * 32 + lane;
+    for (int jj = 0; jj < MK; ++jj) {
+      const int rel = w * 32 * MK + jj * 32 + lane;
       const bool ok = rel < L;
       key[jj] = ok ? a[lo + rel] : K(0);
       if (PAIRS) val[jj] = ok ? av[lo + rel] : 0u;
       dr[jj] = ok ? digit_of(key[jj], g) : 256u;
     }
-    warp_rank<KPT, false>(dr, whist + w * 256);
+    warp_rank<MK, false>(dr, whist + w * 256);
     __syncthreads();
     uint32_t run = 0;
 #pragma unroll
@@ -1571,7 +1576,7 @@ struct Phases {
     s_lstart[threadIdx.x] = block_excl_scan(run, s_warp, &tot);
     __syncthreads();
 #pragma unroll
-    for (int jj = 0; jj < KPT; ++jj) {
+    for (int jj = 0; jj < MK; ++jj) {
       const uint32_t dgt = dr[jj] & 0xffffu;
       if (dgt < 256) {
         const int pos = lo + s_lstart[dgt] + whist[w * 256 + dgt] + (dr[jj] >> 16);
@@ -1586,19 +1591,24 @@ struct Phases {
   // whole input when n <= C): a stack of ranges; each range takes its top
   // passes over the non-constant digits, small sub-buckets are sorted at
   // once, larger ones are pushed back on the stack (recursion).
-  static __device__ void mid(const Params<K>& P, uint32_t* sm) {
+  // CAP: the largest bucket this instantiation holds; it takes the queued
+  // buckets with len_lo < len <= CAP (k_mid_s: up to MID_CAP_S at 4 CTAs/SM,
+  // k_mid: the rest at 2 CTAs/SM)
+  template <int CAP>
+  static __device__ void mid(const Params<K>& P, uint32_t* sm, int len_lo) {
+    constexpr int MK = CAP / THREADS;
     Ctl* c = P.ctl;
     const uint32_t total = min(c->mid_count, P.mid_cap);
     K* S0 = reinterpret_cast<K*>(sm);
-    K* S1 = S0 + MID_CAP;
-    V* V0 = reinterpret_cast<V*>(S1 + MID_CAP);
-    V* V1 = PAIRS ? V0 + MID_CAP : V0;
-    CT* cmp = reinterpret_cast<CT*>(PAIRS ? (void*)(V1 + MID_CAP) : (void*)V0);
-    uint32_t* whist = reinterpret_cast<uint32_t*>(cmp + MID_CAP + 8);
+    K* S1 = S0 + CAP;
+    V* V0 = reinterpret_cast<V*>(S1 + CAP);
+    V* V1 = PAIRS ? V0 + CAP : V0;
+    CT* cmp = reinterpret_cast<CT*>(PAIRS ? (void*)(V1 + CAP) : (void*)V0);
+    uint32_t* whist = reinterpret_cast<uint32_t*>(cmp + CAP + 8);
     uint32_t* wmask = whist + WARPS * 256;  // 2*WARPS*256, kept zero between uses
     uint32_t* s_lstart = wmask + 2 * WARPS * 256;
-    uint32_t* bm = s_lstart + 256;                   // MID_CAP/32 + 8 words
-    uint2* stack = reinterpret_cast<uint2*>(bm + MID_CAP / 32 + 8);  // 512 entries
+    uint32_t* bm = s_lstart + 256;                   // CAP/32 + 8 words
+    uint2* stack = reinterpret_cast<uint2*>(bm + CAP / 32 + 8);  // 512 entries
     uint32_t* s_misc = reinterpret_cast<uint32_t*>(stack + 512);     // 32 words
     unsigned long long* s_diff = reinterpret_cast<unsigned long long*>(s_misc + 16);
     const int nd = (int)P.n_d;
@@ -1610,6 +1620,7 @@ struct Phases {
     for (uint32_t e = blockIdx.x; e < total; e += gridDim.x) {
       const MidE me = P.midq[e];
       const int len = me.len;
+      if (len <= len_lo || len > CAP) continue;  // the other instantiation's bucket
       const K* X = me.buf ? P.B : P.A;
       const V* Xv = me.buf ? P.Bv : P.Av;
       if (me.hi < 0) {  // digits exhausted: a constant bucket, sorted (Alg. 2 l.17-18)
@@ -1669,7 +1680,7 @@ struct Phases {
           for (int dd = hn; dd >= 0 && ng < pmax; --dd)
             if ((diff >> (8 * dd)) & 255ull) gd[ng++] = dd;
           for (int x = ng - 1; x >= 0; --x) {  // least significant of the group first
-            smem_pass(S0, S1, V0, V1, lo, L, gd[x], whist, wmask, s_lstart, s_misc + 8);
+            smem_pass<MK>(S0, S1, V0, V1, lo, L, gd[x], whist, wmask, s_lstart, s_misc + 8);
             for (int i = threadIdx.x; i < L; i += THREADS) {
               S0[lo + i] = S1[lo + i];
               if (PAIRS) V0[lo + i] = V1[lo + i];
@@ -1714,12 +1725,12 @@ struct Phases {
           }
         }
         __syncthreads();
-        // ranks (keys kept in registers, <= KPT per thread)
-        K key[KPT];
-        V val[KPT];
-        int dst[KPT];
+        // ranks (keys kept in registers, <= MK per thread)
+        K key[MK];
+        V val[MK];
+        int dst[MK];
 #pragma unroll
-        for (int m = 0; m < KPT; ++m) {
+        for (int m = 0; m < MK; ++m) {
           const int i = lo + threadIdx.x + THREADS * m;
           dst[m] = -1;
           if (threadIdx.x + THREADS * m < L) {
@@ -1735,7 +1746,7 @@ struct Phases {
         }
         __syncthreads();
 #pragma unroll
-        for (int m = 0; m < KPT; ++m) {
+        for (int m = 0; m < MK; ++m) {
           if (dst[m] >= 0) {
             S0[dst[m]] = key[m];
             if (PAIRS) V0[dst[m]] = val[m];
