@@ -28,7 +28,8 @@ namespace dfr {
 
 // ------------------------------------------------------------------ kernels
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params<K> P, uint32_t n) {
+__global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params<K> P, uint32_t n,
+                                                  int plan_now = 1) {
   extern __shared__ __align__(16) uint32_t sm[];
   Ctl* c = P.ctl;
   if (threadIdx.x == 0) {
@@ -43,6 +44,7 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
     s.buf = P.fuse ? 1u : 0u;  // fused level 0: the histogram kernel copies A to B first
     P.segq[1][0] = s;
   }
+  if (!plan_now) return;  // small inputs: k_levels plans level 0 itself
   __syncthreads();
   Phases<K, PAIRS>::plan(P, sm);
 }
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(THREADS) k_levels(const __grid_constant__ Para
   extern __shared__ __align__(16) uint32_t sm[];
   cg::grid_group grid = cg::this_grid();
   using Ph = Phases<K, PAIRS>;
-  for (int level = 1; level < 2 * P.D; ++level) {
+  for (int level = 0; level < 2 * P.D; ++level) {  // an iteration bound (depth <= D)
     if (*(volatile uint32_t*)&P.ctl->next_count == 0) break;
     grid.sync();
     if (blockIdx.x == 0) Ph::plan(P, sm);
@@ -403,7 +405,29 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
   const int sms = dv.sms;
   const PhaseEv pe{cfg ? cfg->phase_events : nullptr, st};
 
-  if (n <= (size_t)MID_CAP) {  // the whole input fits one on-chip DFR
+  if (n > (size_t)MID_CAP && n <= (size_t)SMALL_N) {
+    // small inputs: every level, level 0 included, in the cooperative
+    // k_levels (one launch instead of one per phase)
+    for (int i = 0; i < DFR_PHASE_LEVELS; ++i) pe.skip(i);
+    pe.begin(DFR_PHASE_LEVELS);
+    k_init<K, PAIRS><<<1, THREADS, 64, st>>>(P, nn, 0);
+    void* args[] = {&P};
+    const uint32_t tiles = (nn + TILE - 1) / TILE;
+    const int g_lv = (int)std::min<uint32_t>((uint32_t)(sms * std::max(1, dv.occ_levels)),
+                                             std::max<uint32_t>(16u, 2u * tiles));
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_levels<K, PAIRS>, g_lv, THREADS,
+                                                args, Ph::SMEM_LEVEL, st);
+    pe.end(DFR_PHASE_LEVELS);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(ws, st);
+      return DFR_ERR_CUDA;
+    }
+    pe.begin(DFR_PHASE_MID);
+    k_mid_s<K, PAIRS><<<sms * std::max(1, dv.occ_mid_s), THREADS, Ph::SMEM_MID_S, st>>>(P);
+    k_mid<K, PAIRS><<<sms * std::max(1, dv.occ_mid), THREADS, Ph::SMEM_MID, st>>>(P, MID_CAP_S);
+    pe.end(DFR_PHASE_MID);
+    g_launches += 4;
+  } else if (n <= (size_t)MID_CAP) {  // the whole input fits one on-chip DFR
     for (int i = 0; i < DFR_PHASE_MID; ++i) pe.skip(i);
     pe.begin(DFR_PHASE_MID);
     k_seed_mid<K, PAIRS><<<1, 1, 0, st>>>(P, nn);

@@ -41,6 +41,10 @@ constexpr int KPT = 16;                  // keys per thread per tile
 constexpr int TILE = THREADS * KPT;      // 4096 keys per tile (hist / deal)
 constexpr int WIN = 1024;                // diversion window (keys) per CTA
 constexpr int MID_CAP = 4096;            // C: buckets N_d < s <= C finish on-chip
+#ifndef DFR_SMALL_N
+#define DFR_SMALL_N (1 << 18)
+#endif
+constexpr int SMALL_N = DFR_SMALL_N;     // inputs up to this size: all levels in k_levels
 constexpr int MID_CAP_S = 1024;          // buckets up to this size: the 4-CTA/SM mid kernel
 constexpr int MAX_ND = 256;              // composite index uses 8 bits
 constexpr int MAX_PASSES = 4;            // top passes per group (p <= 3 for n < 2^30)
