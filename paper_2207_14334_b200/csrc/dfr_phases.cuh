@@ -824,6 +824,7 @@ struct Phases {
   static constexpr uint16_t H_INF = 0x7c00;   // +inf: never below a composite
   static constexpr uint16_t H_BASE = 0x0400;  // smallest positive normal fp16
   static constexpr uint32_t DV_NONE = 0xffffffffu;
+  static constexpr uint32_t DV_HOLE = 0xffffu;  // order slot not filled (window positions < WIN)
   static constexpr int DV_NT = 128;           // threads of the stand-alone divert kernel
   static constexpr size_t DV_WIN_BYTES = WIN * sizeof(K) + (PAIRS ? WIN * 4 : 0);
   static constexpr int DV_CMP = 4 * WIN + 64;  // halves
@@ -968,15 +969,29 @@ struct Phases {
     return lo ? bl : (mid ? bmid : (hi ? bh : 96));
   }
 
-  // warp-wide exact re-rank of every bucket flagged in bmk (lanes' info)
-  static __device__ __noinline__ void rerank_flagged(uint32_t sk_a, uint32_t order_a, uint32_t bmk,
-                                                     uint32_t info, bool b) {
+  // warp-wide exact re-rank of every bucket flagged in bmk (lanes' info),
+  // then its slots written out again (a bucket that straddles two warps is
+  // done by both, with identical results)
+  static __device__ __noinline__ void fixup_flagged(uint32_t sk_a, uint32_t sv_a, uint32_t order_a,
+                                                    uint32_t bmk, uint32_t info, bool b, K* outk,
+                                                    V* outv) {
+    const int lane = threadIdx.x & 31;
     while (bmk) {
       const uint32_t inf = __shfl_sync(0xffffffffu, info, __ffs(bmk) - 1);
-      bmk &= ~__ballot_sync(0xffffffffu, b && (info & 0xffffffu) == (inf & 0xffffffu));
-      rerank_exact(sk_a, order_a, inf & 0xfff, (inf & 0xfff) + ((inf >> 12) & 0x1ff));
+      bmk &= ~__ballot_sync(0xffffffffu, b && (info & 0xfffu) == (inf & 0xfffu));
+      const int bs = inf & 0xfff, be = bs + ((inf >> 12) & 0x1ff);
+      rerank_exact(sk_a, order_a, bs, be);
+      __syncwarp();
+      for (int j = bs + lane; j < be; j += 32) {
+        const uint32_t src = lds16(order_a + 2 * j);
+        outk[j] = ldsk<K>(sk_a + sizeof(K) * src);
+        if (PAIRS) outv[j] = lds32(sv_a + 4 * src);
+      }
+      __syncwarp();
     }
   }
+
+
 
   // Positions: warp w holds the contiguous range [w*WPW, (w+1)*WPW) of the
   // window, 32 consecutive positions per step m.  The bucket-start ballot
@@ -1069,6 +1084,7 @@ struct Phases {
           const uint32_t c16 = comp.template get<LOSSY>(ldsk<K>(sk_a + KB * i), (uint32_t)(i - bs));
           mev[m >> 1] |= c16 << (16 * (m & 1));
           sts16(cmp_a + 2 * (3 * bs + i), c16);
+          if (LOSSY) sts16(order_a + 2 * i, DV_HOLE);  // slot i: filled in C unless a tie
         }
         lg |= (uint32_t)(own && !small && i == bs) << m;
       }
@@ -1091,6 +1107,7 @@ struct Phases {
           const uint32_t c16 = comp.template get<LOSSY>(ldsk<K>(sk_a + KB * i), (uint32_t)(i - bs));
           mev[m >> 1] |= c16 << (16 * (m & 1));
           sts16(cmp_a + 2 * (3 * bs + i), c16);
+          if (LOSSY) sts16(order_a + 2 * i, DV_HOLE);  // slot i: filled in C unless a tie
         }
         lg |= (uint32_t)(own && !small && i == bs) << m;
       }
@@ -1127,37 +1144,38 @@ struct Phases {
         info[m] |= rk << 24;
       }
     }
-    // ---- D: tie check (lossy composites): a slot claimed by another key
-    if (LOSSY) {
-      __syncthreads();
-      uint32_t badm = 0;
-#pragma unroll
-      for (int m = 0; m < DKPT; ++m) {
-        const int i = wbase + 32 * m + lane;
-        if (info[m] != DV_NONE)
-          badm |= (uint32_t)(lds16(order_a + 2 * ((info[m] & 0xfff) + (info[m] >> 24))) != (uint32_t)i) << m;
-      }
-      if (__syncthreads_or(badm != 0)) {
-#pragma unroll
-        for (int m = 0; m < DKPT; ++m) {
-          const bool b = (badm >> m) & 1u;
-          const uint32_t bmk = __ballot_sync(0xffffffffu, b);
-          if (bmk) rerank_flagged(sk_a, order_a, bmk, info[m], b);
-        }
-      }
-    }
     __syncthreads();
-    // ---- E: coalesced write of every owned slot
+    // ---- E: coalesced write of every owned slot.  (lossy) Two keys with
+    // equal composites take the same rank, which leaves a slot of their
+    // bucket unfilled: the lane that finds the hole flags the bucket
     K* outk = P.A + s.start + r0;
     V* outv = P.Av + s.start + r0;
+    uint32_t hole = 0;
 #pragma unroll
     for (int m = 0; m < DKPT; ++m) {
       if (info[m] != DV_NONE) {
         const int j = wbase + 32 * m + lane;
         const uint32_t src = lds16(order_a + 2 * j);
-        outk[j] = ldsk<K>(sk_a + KB * src);
-        if (PAIRS) outv[j] = lds32(sv_a + 4 * src);
+        if (LOSSY && src == DV_HOLE) {
+          hole |= 1u << m;
+        } else {
+          outk[j] = ldsk<K>(sk_a + KB * src);
+          if (PAIRS) outv[j] = lds32(sv_a + 4 * src);
+        }
       }
+    }
+    // ---- D: (rare) flagged buckets re-ranked exactly on the full keys and
+    // written again; the barrier also frees the window, composites and order
+    if (LOSSY && __syncthreads_or(hole != 0)) {
+#pragma unroll
+      for (int m = 0; m < DKPT; ++m) {
+        const bool b = (hole >> m) & 1u;
+        const uint32_t bmk = __ballot_sync(0xffffffffu, b);
+        if (bmk) fixup_flagged(sk_a, sv_a, order_a, bmk, info[m], b, outk, outv);
+      }
+      __syncthreads();
+    } else if (!LOSSY) {
+      __syncthreads();
     }
   }
 
@@ -1253,7 +1271,7 @@ struct Phases {
         if (edge) divert_window<NT, true, true>(P, s, S, sk_a, sv_a, r0, off, comp);
         else      divert_window<NT, true, false>(P, s, S, sk_a, sv_a, r0, off, comp);
       }
-      __syncthreads();  // window buffer, composites and order free
+      // divert_window ends on a barrier: window buffer, composites and order free
       if (threadIdx.x == 0) divert_prefetch(P, q, nseg, total, ch + gridDim.x, S, 0);
       __syncthreads();  // the next window's segment / tma flag visible
     }
