@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(Phases<K, false>::SC_NT, 3) k_scatter_fh(const
 }
 
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(Phases<K, PAIRS>::DV_NT, 10) k_divert(const __grid_constant__ Params<K> P) {
+__global__ void __launch_bounds__(Phases<K, PAIRS>::DV_NT, DFR_DV_MINB) k_divert(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
   Phases<K, PAIRS>::template divert<Phases<K, PAIRS>::DV_NT>(P, sm);
 }

@@ -25,6 +25,9 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_RANK_G
 #define DFR_RANK_G 4  // keys whose peer masks are computed together in warp_rank
 #endif
+#ifndef DFR_HIST_U
+#define DFR_HIST_U 8  // histogram: 16-byte loads in flight per thread
+#endif
 #ifndef DFR_LB
 #define DFR_LB 8  // look-back predecessors loaded per round trip
 #endif
@@ -39,7 +42,10 @@ static_assert(DFR_LB <= LB_PAD, "look-back pad");
 constexpr int WO_UNROLL = DFR_WO_UNROLL, DV_CU = DFR_DV_CU;
 constexpr int KPT = 16;                  // keys per thread per tile
 constexpr int TILE = THREADS * KPT;      // 4096 keys per tile (hist / deal)
-constexpr int WIN = 1024;                // diversion window (keys) per CTA
+#ifndef DFR_WIN
+#define DFR_WIN 1024
+#endif
+constexpr int WIN = DFR_WIN;             // diversion window (keys) per CTA
 constexpr int MID_CAP = 4096;            // C: buckets N_d < s <= C finish on-chip
 #ifndef DFR_SMALL_N
 #define DFR_SMALL_N (1 << 18)

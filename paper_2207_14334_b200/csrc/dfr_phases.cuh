@@ -191,7 +191,7 @@ struct Phases {
     if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0 && (reinterpret_cast<uintptr_t>(cp) & 15) == 0) {
       const uint32_t nv = cnt / VEC;
       const uint4* vp = reinterpret_cast<const uint4*>(tp);
-      constexpr int U = 4;  // 4 independent 16-byte loads in flight per thread
+      constexpr int U = DFR_HIST_U;  // independent 16-byte loads in flight per thread
       uint32_t vb = 0;
       for (; vb + U * THREADS <= nv; vb += U * THREADS) {  // full blocks: no bounds checks
         uint4 x[U];
@@ -825,7 +825,11 @@ struct Phases {
   static constexpr uint16_t H_BASE = 0x0400;  // smallest positive normal fp16
   static constexpr uint32_t DV_NONE = 0xffffffffu;
   static constexpr uint32_t DV_HOLE = 0xffffu;  // order slot not filled (window positions < WIN)
-  static constexpr int DV_NT = 128;           // threads of the stand-alone divert kernel
+#ifndef DFR_DV_NT
+#define DFR_DV_NT 128
+#define DFR_DV_MINB 10
+#endif
+  static constexpr int DV_NT = DFR_DV_NT;     // threads of the stand-alone divert kernel
   static constexpr size_t DV_WIN_BYTES = WIN * sizeof(K) + (PAIRS ? WIN * 4 : 0);
   static constexpr int DV_CMP = 4 * WIN + 64;  // halves
 
