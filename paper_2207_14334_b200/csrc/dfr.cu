@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(THREADS) k_init_stage(Params<K> P, uint32_t n,
 }
 
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(THREADS) k_hist(const __grid_constant__ Params<K> P) {
+__global__ void __launch_bounds__(THREADS, DFR_HIST_MINB) k_hist(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
   Phases<K, PAIRS>::hist(P, sm);
 }
