@@ -191,7 +191,10 @@ struct Phases {
     if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0 && (reinterpret_cast<uintptr_t>(cp) & 15) == 0) {
       const uint32_t nv = cnt / VEC;
       const uint4* vp = reinterpret_cast<const uint4*>(tp);
-      constexpr int U = DFR_HIST_U;  // independent 16-byte loads in flight per thread
+      // independent 16-byte loads in flight per thread; a full block is at
+      // most one tile (u32 keys: 4)
+      constexpr int U_TILE = TILE * (int)sizeof(K) / 16 / THREADS;
+      constexpr int U = DFR_HIST_U < U_TILE ? DFR_HIST_U : U_TILE;
       uint32_t vb = 0;
       for (; vb + U * THREADS <= nv; vb += U * THREADS) {  // full blocks: no bounds checks
         uint4 x[U];
