@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--case", default="c5-uniform", help="datagen case (default: the headline)")
     ap.add_argument("--n", type=int, default=None, help="override the case size")
     ap.add_argument("--quick", action="store_true", help="skip e2e and cpu_baseline (for ncu runs)")
+    ap.add_argument("--phase-events", default="all", choices=["all", "deal", "none"],
+                    help="phases timed with CUDA events inside the timed region (events between "
+                         "kernels stop programmatic dependent launch from overlapping them)")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     return ap.parse_args()
 
@@ -216,10 +219,14 @@ def run_dfr(args, rank, world, local_rank):
     restore = nbuf < K + W  # not enough HBM for a copy per step: restore between steps
     stream = torch.cuda.current_stream()
     nph = len(dfr.PHASES)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nph)] for _ in range(K)]
+    timed = [args.phase_events == "all" or (args.phase_events == "deal" and name.startswith("scatter"))
+             for name in dfr.PHASES]
+    evs = [[torch.cuda.Event(enable_timing=True) if timed[e // 2] else None for e in range(2 * nph)]
+           for _ in range(K)]
     for row in evs:  # torch creates the CUDA event lazily, on its first record
         for e in row:
-            e.record(stream)
+            if e is not None:
+                e.record(stream)
 
     def sort_step(i, ev=None):
         b = bufs[i % nbuf]
@@ -269,7 +276,9 @@ def run_dfr(args, rank, world, local_rank):
     # per-phase device times (CUDA events recorded by the library on this stream)
     phase_ms = {}
     for p, name in enumerate(dfr.PHASES):
-        phase_ms[name] = statistics.mean(evs[i][2 * p].elapsed_time(evs[i][2 * p + 1]) for i in range(K))
+        if timed[p]:
+            phase_ms[name] = statistics.mean(evs[i][2 * p].elapsed_time(evs[i][2 * p + 1])
+                                             for i in range(K))
 
     # verification of the last output: non-decreasing + same multiset as the input
     last = bufs[(W + K - 1) % nbuf]
@@ -282,9 +291,10 @@ def run_dfr(args, rank, world, local_rank):
     peak, peak_src = peak_hbm()
 
     # roofline of the dominant kernel (the stable deal, k_scatter)
-    smax = max(phase_ms[f"scatter{j}"] for j in range(4))
-    sc = [phase_ms[f"scatter{j}"] for j in range(4) if phase_ms[f"scatter{j}"] > 0.05 * smax]
-    dominant = max(phase_ms, key=lambda k: phase_ms[k])
+    smax = max(phase_ms.get(f"scatter{j}", 0.0) for j in range(4))
+    sc = [phase_ms[f"scatter{j}"] for j in range(4)
+          if smax > 0 and phase_ms[f"scatter{j}"] > 0.05 * smax]
+    dominant = max(phase_ms, key=lambda k: phase_ms[k]) if phase_ms else None
     pass_bytes = n * 2 * (kb + vb)
     sc_ms = statistics.mean(sc) if sc else None
     achieved = pass_bytes / (sc_ms / 1e3) / 1e9 if sc_ms else None

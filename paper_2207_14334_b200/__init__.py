@@ -123,11 +123,13 @@ def _dev_tensor(t, widths):
 
 
 def _cfg(n_d, skip_trivial, events=None, fused=False):
-    """events: None or a sequence of 2*len(PHASES) torch.cuda.Event(enable_timing=True).
+    """events: None or a sequence of 2*len(PHASES) torch.cuda.Event(enable_timing=True)
+    (None entries: that phase is not timed).
     fused=True asks for the fused last deal + diversion (dfr_config.fused_last_pass)."""
     c = Config(int(n_d), 1 if skip_trivial else 0, None, 1 if fused else 0)
     if events is not None:
-        arr = (ctypes.c_void_p * len(events))(*[int(e.cuda_event) for e in events])
+        arr = (ctypes.c_void_p * len(events))(*[int(e.cuda_event) if e is not None else 0
+                                                  for e in events])
         c._keep = arr
         c.phase_events = ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p))
     return c

@@ -77,12 +77,14 @@ __global__ void __launch_bounds__(THREADS) k_init_stage(Params<K> P, uint32_t n,
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(THREADS, DFR_HIST_MINB) k_hist(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
+  pdl_enter();
   Phases<K, PAIRS>::hist(P, sm);
 }
 
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(THREADS) k_plan2(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
+  pdl_enter();
   Phases<K, PAIRS>::plan2(P, sm);
 }
 
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(THREADS) k_plan2(const __grid_constant__ Param
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(THREADS) k_lplan(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
+  pdl_enter();
   Ctl* c = P.ctl;
   if (*(volatile uint32_t*)&c->next_count == 0) {
     if (threadIdx.x == 0) {
@@ -108,6 +111,7 @@ __global__ void __launch_bounds__(THREADS) k_lplan(const __grid_constant__ Param
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(Phases<K, PAIRS>::SC_NT, 4) k_scatter(const __grid_constant__ Params<K> P, int j) {
   extern __shared__ __align__(16) uint32_t sm[];
+  pdl_enter();
   Phases<K, PAIRS>::template scatter<Phases<K, PAIRS>::SC_NT, false, true>(P, j, sm);
 }
 
@@ -115,35 +119,41 @@ __global__ void __launch_bounds__(Phases<K, PAIRS>::SC_NT, 4) k_scatter(const __
 template <class K>
 __global__ void __launch_bounds__(Phases<K, false>::SC_NT, 3) k_scatter_fh(const __grid_constant__ Params<K> P, int j) {
   extern __shared__ __align__(16) uint32_t sm[];
+  pdl_enter();
   Phases<K, false>::template scatter<Phases<K, false>::SC_NT, true>(P, j, sm);
 }
 
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(Phases<K, PAIRS>::DV_NT, DFR_DV_MINB) k_divert(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
+  pdl_enter();
   Phases<K, PAIRS>::template divert<Phases<K, PAIRS>::DV_NT>(P, sm);
 }
 
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(1024) k_fplan(const __grid_constant__ Params<K> P) {
+  pdl_enter();
   Phases<K, PAIRS>::fplan(P);
 }
 
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(Phases<K, PAIRS>::FNT, 2) k_fused(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
+  pdl_enter();
   Phases<K, PAIRS>::fused(P, sm);
 }
 
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(THREADS, 2) k_mid(const __grid_constant__ Params<K> P, int len_lo) {
   extern __shared__ __align__(16) uint32_t sm[];
+  pdl_enter();
   Phases<K, PAIRS>::template mid<MID_CAP>(P, sm, len_lo);
 }
 // the mid buckets of at most MID_CAP_S keys, at 4 CTAs/SM
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(THREADS, 4) k_mid_s(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
+  pdl_enter();
   Phases<K, PAIRS>::template mid<MID_CAP_S>(P, sm, 0);
 }
 
@@ -188,6 +198,27 @@ __global__ void k_seed_mid(Params<K> P, uint32_t n) {
 }
 
 // ------------------------------------------------------------------ host
+// launch with programmatic stream serialization (see pdl_enter)
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+#ifdef DFR_NO_PDL
+  cfg.numAttrs = 0;
+#else
+  cfg.numAttrs = 1;
+#endif
+  cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 static std::atomic<unsigned long long> g_launches{0};
 
 #ifdef DFR_DEBUG
@@ -423,15 +454,15 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
       return DFR_ERR_CUDA;
     }
     pe.begin(DFR_PHASE_MID);
-    k_mid_s<K, PAIRS><<<sms * std::max(1, dv.occ_mid_s), THREADS, Ph::SMEM_MID_S, st>>>(P);
-    k_mid<K, PAIRS><<<sms * std::max(1, dv.occ_mid), THREADS, Ph::SMEM_MID, st>>>(P, MID_CAP_S);
+    launch_pdl(k_mid_s<K, PAIRS>, sms * std::max(1, dv.occ_mid_s), THREADS, Ph::SMEM_MID_S, st, P);
+    launch_pdl(k_mid<K, PAIRS>, sms * std::max(1, dv.occ_mid), THREADS, Ph::SMEM_MID, st, P, MID_CAP_S);
     pe.end(DFR_PHASE_MID);
     g_launches += 4;
   } else if (n <= (size_t)MID_CAP) {  // the whole input fits one on-chip DFR
     for (int i = 0; i < DFR_PHASE_MID; ++i) pe.skip(i);
     pe.begin(DFR_PHASE_MID);
     k_seed_mid<K, PAIRS><<<1, 1, 0, st>>>(P, nn);
-    k_mid<K, PAIRS><<<1, THREADS, Ph::SMEM_MID, st>>>(P, 0);
+    launch_pdl(k_mid<K, PAIRS>, 1, THREADS, Ph::SMEM_MID, st, P, 0);
     pe.end(DFR_PHASE_MID);
     g_launches += 2;
   } else {
@@ -439,10 +470,10 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
     pe.begin(DFR_PHASE_HIST);
     k_init<K, PAIRS><<<1, THREADS, 64, st>>>(P, nn);
     const int g_hist = (int)std::min<uint32_t>(tiles, (uint32_t)(sms * std::max(1, dv.occ_hist)));
-    k_hist<K, PAIRS><<<g_hist, THREADS, Ph::SMEM_HIST, st>>>(P);
+    launch_pdl(k_hist<K, PAIRS>, g_hist, THREADS, Ph::SMEM_HIST, st, P);
     pe.end(DFR_PHASE_HIST);
     pe.begin(DFR_PHASE_PLAN);
-    k_plan2<K, PAIRS><<<1, THREADS, 64, st>>>(P);
+    launch_pdl(k_plan2<K, PAIRS>, 1, THREADS, 64, st, P);
     pe.end(DFR_PHASE_PLAN);
     const int g_sc = (int)std::min<uint32_t>(tiles, (uint32_t)(sms * std::max(1, dv.occ_scatter)));
     for (int j = 0; j < MAX_PASSES; ++j) {
@@ -452,31 +483,31 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
       }
       pe.begin(DFR_PHASE_SCATTER0 + j);
       if (fuse && j == 2) {  // run-aligned tiles, then the fused last deal + diversion
-        k_fplan<K, PAIRS><<<1, 1024, 0, st>>>(P);
+        launch_pdl(k_fplan<K, PAIRS>, 1, 1024, 0, st, P);
         const int g_f = sms * std::max(1, dv.occ_fused);
-        k_fused<K, PAIRS><<<g_f, Ph::FNT, Ph::SMEM_FUSED, st>>>(P);
+        launch_pdl(k_fused<K, PAIRS>, g_f, Ph::FNT, Ph::SMEM_FUSED, st, P);
         g_launches += 2;
       }
       if (fuse && j == 1 && !PAIRS)
-        k_scatter_fh<K><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER, st>>>(P, j);
+        launch_pdl(k_scatter_fh<K>, g_sc, Ph::SC_NT, Ph::SMEM_SCATTER, st, P, j);
       else
-        k_scatter<K, PAIRS><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER_P, st>>>(P, j);  // no-op when fused
+        launch_pdl(k_scatter<K, PAIRS>, g_sc, Ph::SC_NT, Ph::SMEM_SCATTER_P, st, P, j);  // no-op when fused
       pe.end(DFR_PHASE_SCATTER0 + j);
     }
     const uint32_t chunks = (nn + P.chunk - 1) / P.chunk;
     const int g_dv = (int)std::min<uint32_t>(chunks, (uint32_t)(sms * std::max(1, dv.occ_divert)));
     pe.begin(DFR_PHASE_DIVERT);
-    k_divert<K, PAIRS><<<g_dv, Ph::DV_NT, Ph::SMEM_DIVERT, st>>>(P);
+    launch_pdl(k_divert<K, PAIRS>, g_dv, Ph::DV_NT, Ph::SMEM_DIVERT, st, P);
     pe.end(DFR_PHASE_DIVERT);
     pe.begin(DFR_PHASE_LEVELS);
     // level 1 through the stand-alone kernels (large recursions: c3, c4,
     // c5-low20 put most of their keys there), levels 2.. in k_levels
-    k_lplan<K, PAIRS><<<1, THREADS, 64, st>>>(P);
-    k_hist<K, PAIRS><<<g_hist, THREADS, Ph::SMEM_HIST, st>>>(P);
-    k_plan2<K, PAIRS><<<4 * sms, THREADS, 64, st>>>(P);  // one block per segment
+    launch_pdl(k_lplan<K, PAIRS>, 1, THREADS, 64, st, P);
+    launch_pdl(k_hist<K, PAIRS>, g_hist, THREADS, Ph::SMEM_HIST, st, P);
+    launch_pdl(k_plan2<K, PAIRS>, 4 * sms, THREADS, 64, st, P);  // one block per segment
     for (int j = 0; j < MAX_PASSES; ++j)
-      k_scatter<K, PAIRS><<<g_sc, Ph::SC_NT, Ph::SMEM_SCATTER_P, st>>>(P, j);
-    k_divert<K, PAIRS><<<g_dv, Ph::DV_NT, Ph::SMEM_DIVERT, st>>>(P);
+      launch_pdl(k_scatter<K, PAIRS>, g_sc, Ph::SC_NT, Ph::SMEM_SCATTER_P, st, P, j);
+    launch_pdl(k_divert<K, PAIRS>, g_dv, Ph::DV_NT, Ph::SMEM_DIVERT, st, P);
     g_launches += 4 + MAX_PASSES;
     void* args[] = {&P};
     const int g_lv = sms * std::max(1, dv.occ_levels);
@@ -489,8 +520,8 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
     }
     pe.begin(DFR_PHASE_MID);
     const int g_mid = sms * std::max(1, dv.occ_mid);
-    k_mid_s<K, PAIRS><<<sms * std::max(1, dv.occ_mid_s), THREADS, Ph::SMEM_MID_S, st>>>(P);
-    k_mid<K, PAIRS><<<g_mid, THREADS, Ph::SMEM_MID, st>>>(P, MID_CAP_S);
+    launch_pdl(k_mid_s<K, PAIRS>, sms * std::max(1, dv.occ_mid_s), THREADS, Ph::SMEM_MID_S, st, P);
+    launch_pdl(k_mid<K, PAIRS>, g_mid, THREADS, Ph::SMEM_MID, st, P, MID_CAP_S);
     pe.end(DFR_PHASE_MID);
     g_launches += 7 + p0;
   }

@@ -435,6 +435,14 @@ __device__ __forceinline__ void coop_copy(T* dst, const T* src, uint32_t n, uint
   }
 }
 
+// programmatic dependent launch: wait for the previous grid in the stream
+// (all its memory operations visible), then let the next grid be scheduled
+// (its CTAs block in their own wait) -- hides kernel-boundary latency
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // binary search: largest i in [0, n) with key(i) <= t (key non-decreasing, key(0) = 0)
 template <class F>
 __device__ __forceinline__ uint32_t upper_index(uint32_t n, uint32_t t, F key) {
