@@ -40,8 +40,10 @@ struct Phases {
   static constexpr size_t SMEM_SCATTER =
       SCATTER_HDR_WORDS * 4 + 2 * TILE * sizeof(K) + (PAIRS ? 2 * TILE * 4 : 0);
   // PERM deal: header | permutation | one tile
+  // (the tile buffers hold the 16-byte aligned superset of a tile: SUP_K / SUP_V)
+  static constexpr int SUP_K = TILE + 2 * (16 / (int)sizeof(K)), SUP_V = TILE + 8;
   static constexpr size_t SMEM_SCATTER_P =
-      SCATTER_HDR_WORDS * 4 + TILE * 2 + TILE * sizeof(K) + (PAIRS ? TILE * 4 : 0);
+      SCATTER_HDR_WORDS * 4 + TILE * 2 + SUP_K * sizeof(K) + (PAIRS ? SUP_V * 4 : 0);
   // 2 windows (+ values) | fp16 composites | order | bitmask, misc, mbarriers
   static constexpr size_t SMEM_DIVERT = 1 * (WIN * sizeof(K) + (PAIRS ? WIN * 4 : 0)) +
                                         (4 * WIN + 64) * 2 + WIN * 2 + (WIN / 32 + 12) * 4 + 16 + 16;
@@ -188,6 +190,22 @@ struct Phases {
   // passes from the scratch buffer, so that the fused last pass lands in A)
   static __device__ __forceinline__ void hist_tile(const K* tp, uint32_t cnt, K kref, int low,
                                                    uint32_t shw, unsigned long long& diff, K* cp) {
+    // a tile at any offset (recursion levels): warp 0 counts the < VEC head
+    // keys before the 16-byte boundary, the rest takes the vector path
+    const uintptr_t mis = reinterpret_cast<uintptr_t>(tp) & 15;
+    if (mis && (mis % sizeof(K)) == 0 && (!cp || (reinterpret_cast<uintptr_t>(cp) & 15) == mis)) {
+      const uint32_t h = min(cnt, (uint32_t)((16 - mis) / sizeof(K)));
+      if (threadIdx.x < 32) {
+        const bool ok = threadIdx.x < h;
+        const K k = ok ? tp[threadIdx.x] : K(0);
+        if (cp && ok) cp[threadIdx.x] = k;
+        if (ok) diff |= (unsigned long long)(k ^ kref);
+        count_key<NP>(shw, k, ok, low);
+      }
+      tp += h;
+      cnt -= h;
+      if (cp) cp += h;
+    }
     if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0 && (reinterpret_cast<uintptr_t>(cp) & 15) == 0) {
       const uint32_t nv = cnt / VEC;
       const uint4* vp = reinterpret_cast<const uint4*>(tp);
@@ -567,7 +585,10 @@ struct Phases {
   // full aligned tile of an active segment, start its TMA bulk load
   // (DEFER: ticket, segment and eligibility only; issue_tile starts the copy
   // later — ti is then final before the caller's next barrier)
-  template <bool DEFER = false>
+  // SUP: the copy covers the 16-byte aligned superset of the tile (the tile
+  // starts koff keys / voff values into the buffer, ti[3] = koff | voff << 8),
+  // so that tiles of segments at any offset (recursion levels) still use TMA
+  template <bool DEFER = false, bool SUP = false>
   static __device__ __forceinline__ void claim_tile(const Params<K>& P, int j, const Seg* q,
                                                     uint32_t nseg, uint32_t total, uint32_t* ti,
                                                     K* kb, V* vb, unsigned long long* bar) {
@@ -583,12 +604,30 @@ struct Phases {
     const uint32_t sb = src_buf(s, j);
     const K* src = (sb ? P.B : P.A) + s.start + lt * TILE;
     const V* srcv = PAIRS ? (sb ? P.Bv : P.Av) + s.start + lt * TILE : nullptr;
-    if ((reinterpret_cast<uintptr_t>(src) & 15) || (PAIRS && (reinterpret_cast<uintptr_t>(srcv) & 15)))
+    if (SUP) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(src), a0 = a & ~(uintptr_t)15;
+      const uintptr_t k0 = reinterpret_cast<uintptr_t>(sb ? P.B : P.A);
+      if (a0 < k0 || a0 + sup_bytes(a - a0, TILE * sizeof(K)) > k0 + (uintptr_t)P.n * sizeof(K)) return;
+      uint32_t off = (uint32_t)((a - a0) / sizeof(K));
+      if (PAIRS) {
+        const uintptr_t b = reinterpret_cast<uintptr_t>(srcv), b0 = b & ~(uintptr_t)15;
+        const uintptr_t v0 = reinterpret_cast<uintptr_t>(sb ? P.Bv : P.Av);
+        if (b0 < v0 || b0 + sup_bytes(b - b0, TILE * 4) > v0 + (uintptr_t)P.n * 4) return;
+        off |= (uint32_t)((b - b0) / 4) << 8;
+      }
+      ti[3] = off;
+    } else if ((reinterpret_cast<uintptr_t>(src) & 15) ||
+               (PAIRS && (reinterpret_cast<uintptr_t>(srcv) & 15))) {
       return;
+    }
     ti[2] = 1;
-    if (!DEFER) issue_tile(P, j, q, ti, kb, vb, bar);
+    if (!DEFER) issue_tile<SUP>(P, j, q, ti, kb, vb, bar);
+  }
+  static __device__ __forceinline__ uint32_t sup_bytes(uintptr_t head, uint32_t bytes) {
+    return (uint32_t)((head + bytes + 15) & ~(uintptr_t)15);
   }
   // thread 0: start the TMA bulk copy of the claimed tile in ti (ti[2] = 1)
+  template <bool SUP = false>
   static __device__ __forceinline__ void issue_tile(const Params<K>& P, int j, const Seg* q,
                                                     const uint32_t* ti, K* kb, V* vb,
                                                     unsigned long long* bar) {
@@ -598,21 +637,31 @@ struct Phases {
     const uint32_t sb = src_buf(s, j);
     const K* src = (sb ? P.B : P.A) + s.start + lt * TILE;
     const V* srcv = PAIRS ? (sb ? P.Bv : P.Av) + s.start + lt * TILE : nullptr;
+    uint32_t kbytes = TILE * sizeof(K), vbytes = TILE * 4;
+    if (SUP) {
+      const uint32_t koff = ti[3] & 0xffu, voff = ti[3] >> 8;
+      kbytes = sup_bytes(koff * sizeof(K), TILE * sizeof(K));
+      src -= koff;
+      if (PAIRS) {
+        vbytes = sup_bytes(voff * 4, TILE * 4);
+        srcv -= voff;
+      }
+    }
     fence_proxy_async();
-    const uint32_t bytes = TILE * sizeof(K) + (PAIRS ? TILE * 4 : 0);
+    const uint32_t bytes = kbytes + (PAIRS ? vbytes : 0);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_u32(kb)),
-        "l"(src), "r"((uint32_t)(TILE * sizeof(K))), "r"(smem_u32(bar))
+        "l"(src), "r"(kbytes), "r"(smem_u32(bar))
         : "memory");
     if (PAIRS)
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
               smem_u32(vb)),
-          "l"(srcv), "r"((uint32_t)(TILE * 4)), "r"(smem_u32(bar))
+          "l"(srcv), "r"(vbytes), "r"(smem_u32(bar))
           : "memory");
   }
 
@@ -639,13 +688,13 @@ struct Phases {
     uint16_t* const perm = reinterpret_cast<uint16_t*>(sm + SCATTER_HDR_WORDS);  // PERM: TILE
     K* const kb0 = PERM ? reinterpret_cast<K*>(perm + TILE)
                         : reinterpret_cast<K*>(sm + SCATTER_HDR_WORDS);  // (1 or 2) x TILE keys
-    V* const vb0 = reinterpret_cast<V*>(kb0 + (PERM ? 1 : 2) * TILE);   // (1 or 2) x TILE values
+    V* const vb0 = reinterpret_cast<V*>(kb0 + (PERM ? SUP_K : 2 * TILE));  // (1 or 2) x TILE values
     uint32_t* status = P.status + (size_t)j * P.status_stride;
     if (threadIdx.x == 0) {
       mbar_init(&bar[0], 1);
       mbar_init(&bar[1], 1);
       fence_mbar_init();
-      claim_tile(P, j, q, nseg, total, ti, kb0, vb0, &bar[0]);
+      claim_tile<false, PERM>(P, j, q, nseg, total, ti, kb0, vb0, &bar[0]);
     }
     uint32_t phases = 0;  // mbarrier parity per buffer
     // the segment record and its bucket-offset row are re-read only when a
@@ -674,12 +723,14 @@ struct Phases {
           bstart = P.hist[(size_t)(s.hist_off + j) * 256 + threadIdx.x];
       }
       const bool tma = ti[cb * 4 + 2] != 0;
-      K* sk = kb0 + cb * TILE;
-      V* sv = vb0 + cb * TILE;
+      const uint32_t sup = (PERM && tma) ? ti[3] : 0u;  // the tile's offset in the aligned copy
+      K* sk = kb0 + cb * TILE + (sup & 0xffu);
+      V* sv = vb0 + cb * TILE + (sup >> 8);
       auto claim_next = [&]() {
         if (threadIdx.x == 0) {
           const int nb = PERM ? 0 : (cb ^ 1);
-          claim_tile(P, j, q, nseg, total, ti + nb * 4, kb0 + nb * TILE, vb0 + nb * TILE, &bar[nb]);
+          claim_tile<false, PERM>(P, j, q, nseg, total, ti + nb * 4, kb0 + nb * TILE, vb0 + nb * TILE,
+                                  &bar[nb]);
         }
       };
       // claim the next tile once this one's prefix is known (tickets in
@@ -688,7 +739,7 @@ struct Phases {
         if (!PERM)
           claim_next();
         else if (threadIdx.x == 0)
-          claim_tile<true>(P, j, q, nseg, total, ti, kb0, vb0, &bar[0]);
+          claim_tile<true, true>(P, j, q, nseg, total, ti, kb0, vb0, &bar[0]);
       };
       if (!pass_active(s, j)) {
         claim_next();
@@ -724,7 +775,7 @@ struct Phases {
         __syncthreads();
         if (threadIdx.x == 0) {
           fence_proxy_async();
-          issue_tile(P, j, q, ti, kb0, vb0, &bar[0]);
+          issue_tile<PERM>(P, j, q, ti, kb0, vb0, &bar[0]);
         }
       }
       fence_proxy_async();  // generic smem accesses before a later TMA into this buffer
