@@ -426,7 +426,7 @@ struct Phases {
                                                    uint32_t t, uint32_t lt, uint32_t cnt, int dg,
                                                    uint32_t* status, K* sk, V* sv, uint32_t* whist,
                                                    int* s_dst, uint32_t* s_warp, K* dst, V* dstv,
-                                                   uint32_t bstart, uint16_t* perm) {
+                                                   uint32_t bstart, uint16_t* perm, uint32_t sup) {
     constexpr int SC_W = SC_NT / 32;
     constexpr int SC_KPT = TILE / SC_NT;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -440,7 +440,7 @@ struct Phases {
 #pragma unroll
     for (int jj = 0; jj < SC_KPT; ++jj) {
       const uint32_t idx = w * 32 * SC_KPT + jj * 32 + lane;
-      key[jj] = sk[idx];
+      key[jj] = sk[(PERM ? (sup & 0xffu) : 0u) + idx];  // PERM: the tile starts koff into sk
       if (PAIRS && !PERM) val[jj] = sv[idx];
       dr[jj] = (FULL || idx < cnt) ? digit_of(key[jj], dg) : 256u;
       if (FULL || idx < cnt) red_add_shared(tc_s + 4 * dr[jj], 1u);  // tile histogram
@@ -512,7 +512,7 @@ struct Phases {
       if (FULL || dgt < 256) {
         const uint32_t pos = mywh[dgt] + (dr[jj] >> 16);
         if (PERM) {
-          perm[pos] = (uint16_t)(w * 32 * SC_KPT + jj * 32 + lane);
+          perm[pos] = (uint16_t)((sup & 0xffu) + w * 32 * SC_KPT + jj * 32 + lane);
         } else {
           sk[pos] = key[jj];
           if (PAIRS) sv[pos] = val[jj];
@@ -570,7 +570,7 @@ struct Phases {
       }
 #endif
       dst[o] = k;
-      if (PAIRS) dstv[o] = sv[src];
+      if (PAIRS) dstv[o] = sv[PERM ? src - (sup & 0xffu) + (sup >> 8) : src];
     }
   }
 
@@ -604,7 +604,11 @@ struct Phases {
     const uint32_t sb = src_buf(s, j);
     const K* src = (sb ? P.B : P.A) + s.start + lt * TILE;
     const V* srcv = PAIRS ? (sb ? P.Bv : P.Av) + s.start + lt * TILE : nullptr;
-    if (SUP) {
+    const bool aligned = !(reinterpret_cast<uintptr_t>(src) & 15) &&
+                         !(PAIRS && (reinterpret_cast<uintptr_t>(srcv) & 15));
+    if (SUP) ti[3] = 0;
+    if (aligned) {
+    } else if (SUP) {
       const uintptr_t a = reinterpret_cast<uintptr_t>(src), a0 = a & ~(uintptr_t)15;
       const uintptr_t k0 = reinterpret_cast<uintptr_t>(sb ? P.B : P.A);
       if (a0 < k0 || a0 + sup_bytes(a - a0, TILE * sizeof(K)) > k0 + (uintptr_t)P.n * sizeof(K)) return;
@@ -616,8 +620,7 @@ struct Phases {
         off |= (uint32_t)((b - b0) / 4) << 8;
       }
       ti[3] = off;
-    } else if ((reinterpret_cast<uintptr_t>(src) & 15) ||
-               (PAIRS && (reinterpret_cast<uintptr_t>(srcv) & 15))) {
+    } else {
       return;
     }
     ti[2] = 1;
@@ -638,7 +641,7 @@ struct Phases {
     const K* src = (sb ? P.B : P.A) + s.start + lt * TILE;
     const V* srcv = PAIRS ? (sb ? P.Bv : P.Av) + s.start + lt * TILE : nullptr;
     uint32_t kbytes = TILE * sizeof(K), vbytes = TILE * 4;
-    if (SUP) {
+    if (SUP && ti[3]) {
       const uint32_t koff = ti[3] & 0xffu, voff = ti[3] >> 8;
       kbytes = sup_bytes(koff * sizeof(K), TILE * sizeof(K));
       src -= koff;
@@ -723,9 +726,9 @@ struct Phases {
           bstart = P.hist[(size_t)(s.hist_off + j) * 256 + threadIdx.x];
       }
       const bool tma = ti[cb * 4 + 2] != 0;
-      const uint32_t sup = (PERM && tma) ? ti[3] : 0u;  // the tile's offset in the aligned copy
-      K* sk = kb0 + cb * TILE + (sup & 0xffu);
-      V* sv = vb0 + cb * TILE + (sup >> 8);
+      const uint32_t sup = (PERM && tma) ? ti[3] : 0u;  // the tile's offsets in the aligned copy
+      K* sk = kb0 + cb * TILE;
+      V* sv = vb0 + cb * TILE;
       auto claim_next = [&]() {
         if (threadIdx.x == 0) {
           const int nb = PERM ? 0 : (cb ^ 1);
@@ -766,10 +769,10 @@ struct Phases {
       }
       if (cnt == (uint32_t)TILE)
         deal_tile<SC_NT, true, FUSEH, PERM>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist,
-                                            s_dst, s_warp, dst, dstv, bstart, perm);
+                                            s_dst, s_warp, dst, dstv, bstart, perm, sup);
       else
         deal_tile<SC_NT, false, FUSEH, PERM>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist,
-                                             s_dst, s_warp, dst, dstv, bstart, perm);
+                                             s_dst, s_warp, dst, dstv, bstart, perm, sup);
       if (PERM) {  // single buffer: refill it once every thread is done with the write-out
         for (int e = threadIdx.x; e < (SC_W + 1) * 256; e += SC_NT) whist[e] = 0;
         __syncthreads();
