@@ -316,9 +316,6 @@ template <bool FULL>
 __device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
   // lanes whose digit equals this lane's: AND over the digit bits of the
   // bit's ballot, complemented where this lane's bit is 0
-#ifdef DFR_EXPERIMENT_NOPEERS
-  if (FULL) return 1u << (threadIdx.x & 31);  // timing experiment only: wrong output
-#endif
 #ifndef DFR_PEERS_C
   // per bit: lop3 -> predicate, vote, predicated not, and (4 SASS instructions)
   uint32_t peers;
@@ -333,7 +330,6 @@ __device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
         " and.b32 t, %1, 64; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
         " and.b32 t, %1, 128; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
         "}" : "=r"(peers) : "r"(d));
-#ifndef DFR_PEERS_C9
   else  // digit 256 marks an empty slot: a ninth bit
     asm("{\n .reg .pred p;\n .reg .b32 v, t;\n"
         " and.b32 t, %1, 1; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; mov.b32 %0, v;\n"
@@ -347,9 +343,6 @@ __device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
         " and.b32 t, %1, 256; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 v, p, 0xffffffff; @!p not.b32 v, v; and.b32 %0, %0, v;\n"
         "}" : "=r"(peers) : "r"(d));
   return peers;
-#else
-  if (FULL) return peers;
-#endif
 #endif
   // C form (-DDFR_PEERS_C; 5 instructions per bit): the bit moved to the sign
   // position, its ballot xor the spread of the lane's own bit marks the lanes

@@ -521,11 +521,7 @@ struct Phases {
     }
     if (dig_thread) {
       uint32_t excl = 0;
-#ifdef DFR_EXPERIMENT_NOLB
-      if (false) {  // timing experiment only: wrong output
-#else
       if (lt > 0) {  // decoupled look-back, up to LB predecessors per round trip
-#endif
         int tt = (int)t - 1;
         while (true) {
           constexpr int LB = DFR_LB;  // predecessors per look-back round trip

@@ -45,6 +45,10 @@ if os.path.exists(rep):
             "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+            "smsp__inst_executed_op_shared_atom.sum",
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum",
+            "smsp__inst_executed_op_global_red.sum",
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
             "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
