@@ -25,6 +25,9 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_RANK_G
 #define DFR_RANK_G 4  // keys whose peer masks are computed together in warp_rank
 #endif
+#ifndef DFR_COLD
+#define DFR_COLD __noinline__  // rare paths called from the diversion's window loop
+#endif
 #ifndef DFR_HIST_MINB
 #define DFR_HIST_MINB 4  // histogram: minimum resident CTAs per SM (register cap)
 #endif

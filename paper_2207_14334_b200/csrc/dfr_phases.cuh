@@ -972,7 +972,7 @@ struct Phases {
 
   // a bucket > N_d starting at segment index rb: find its end (gallop over
   // the segment), queue it (Alg. 4 l.9-11)
-  static __device__ __noinline__ void divert_large(const Params<K>& P, const Seg& s, int rb,
+  static __device__ DFR_COLD void divert_large(const Params<K>& P, const Seg& s, int rb,
                                                    int known, int shift) {
     const K* xs = (s.final_buf ? P.B : P.A) + s.start;
     const K pre = xs[rb] >> shift;
@@ -1001,7 +1001,7 @@ struct Phases {
   }
 
   // exact stable ranks of the bucket [bs, be) of the window, by one warp
-  static __device__ __noinline__ void rerank_exact(uint32_t sk_a, uint32_t order_a, int bs, int be) {
+  static __device__ DFR_COLD void rerank_exact(uint32_t sk_a, uint32_t order_a, int bs, int be) {
     const int lane = threadIdx.x & 31;
     for (int y = bs + lane; y < be; y += 32) {
       const K ky = ldsk<K>(sk_a + sizeof(K) * y);
@@ -1029,7 +1029,7 @@ struct Phases {
   // warp-wide exact re-rank of every bucket flagged in bmk (lanes' info),
   // then its slots written out again (a bucket that straddles two warps is
   // done by both, with identical results)
-  static __device__ __noinline__ void fixup_flagged(uint32_t sk_a, uint32_t sv_a, uint32_t order_a,
+  static __device__ DFR_COLD void fixup_flagged(uint32_t sk_a, uint32_t sv_a, uint32_t order_a,
                                                     uint32_t bmk, uint32_t info, bool b, K* outk,
                                                     V* outv) {
     const int lane = threadIdx.x & 31;
