@@ -11,6 +11,6 @@ cat gpurun_out/${TAG}_bench.json
 python bench.py --quick --steps 2 --warmup 1 > gpurun_out/${TAG}_plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   -c 40 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --quick --steps 2 --warmup 1 > gpurun_out/${TAG}_ncu_list.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_scatter|k_divert|k_hist" -s 0 -c 3 \
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_scatter|k_divert|k_hist" -s 0 -c 5 \
   -o gpurun_out/${TAG}_full python bench.py --quick --steps 1 --warmup 1 > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "done rc=$?"
