@@ -1638,7 +1638,7 @@ struct Phases {
       if (PAIRS) val[jj] = ok ? av[lo + rel] : 0u;
       dr[jj] = ok ? digit_of(key[jj], g) : 256u;
     }
-    warp_rank<MK, false>(dr, whist + w * 256);
+    if (w * 32 * MK < L) warp_rank<MK, false>(dr, whist + w * 256);  // warps past the range idle
     __syncthreads();
     uint32_t run = 0;
 #pragma unroll
