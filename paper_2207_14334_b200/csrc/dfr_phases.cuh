@@ -1706,9 +1706,25 @@ struct Phases {
           }
         continue;
       }
-      for (int i = threadIdx.x; i < len; i += THREADS) {
-        S0[i] = X[me.start + i];
-        if (PAIRS) V0[i] = Xv[me.start + i];
+      {  // all MK loads of a thread in flight before its shared-memory stores
+        K pk[MK];
+        V pv[MK];
+#pragma unroll
+        for (int m = 0; m < MK; ++m) {
+          const int i = threadIdx.x + THREADS * m;
+          if (i < len) {
+            pk[m] = X[me.start + i];
+            if (PAIRS) pv[m] = Xv[me.start + i];
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < MK; ++m) {
+          const int i = threadIdx.x + THREADS * m;
+          if (i < len) {
+            S0[i] = pk[m];
+            if (PAIRS) V0[i] = pv[m];
+          }
+        }
       }
       if (threadIdx.x == 0) {
         stack[0] = make_uint2((uint32_t)len << 16, (uint32_t)(me.hi + 1));
