@@ -318,9 +318,13 @@ struct Phases {
       }
       const uint32_t lt = t - s.tile0;
       const uint32_t base = s.start + lt * TILE;
-      const uint32_t cnt = min((uint32_t)TILE, s.len - lt * TILE);
+      // up to HT deal tiles of the segment per step (fewer per-step overheads)
+      const uint32_t nt = min(min((uint32_t)DFR_HIST_TILES, t1 - t), s.tile0 + s.ntiles - t);
+      const uint32_t cnt = min(nt * TILE, s.len - lt * TILE);
       for (uint32_t j = 0; j < s.p; ++j)
-        P.status[j * P.status_stride + (size_t)t * 256 + threadIdx.x] = 0;
+        for (uint32_t u = 0; u < nt; ++u)
+          P.status[j * P.status_stride + (size_t)(t + u) * 256 + threadIdx.x] = 0;
+      t += nt - 1;
       const K* src = (s.buf && !fcopy) ? P.B : P.A;  // fused level 0: the input is still in A
       const K kref = src[s.start];
       const K* tp = src + base;
