@@ -31,6 +31,9 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_HIST_MINB
 #define DFR_HIST_MINB 4  // histogram: minimum resident CTAs per SM (register cap)
 #endif
+#ifndef DFR_CLAIM_AFTER_BARRIER
+#define DFR_CLAIM_AFTER_BARRIER 1  // deal: claim the next ticket after the look-back barrier
+#endif
 #ifndef DFR_HIST_TILES
 #define DFR_HIST_TILES 8  // histogram: deal tiles counted per step of its tile loop
 #endif

@@ -555,8 +555,13 @@ struct Phases {
       // run offset of the digit relative to the tile's local offsets, mod 2^32
       s_dst[dd] = (int)(s.start + bstart + excl - lstart);
     }
+#if DFR_CLAIM_AFTER_BARRIER
+    __syncthreads();
+    after_lookback();  // thread 0: claim the next tile (its atomic overlaps the write-out)
+#else
     after_lookback();  // thread 0: claim the next tile, start its TMA load
     __syncthreads();
+#endif
     // coalesced write of each digit run
 #pragma unroll WO_UNROLL
     for (uint32_t i = threadIdx.x; i < (FULL ? (uint32_t)TILE : cnt); i += SC_NT) {
