@@ -47,7 +47,7 @@ constexpr int WARPS = THREADS / 32;
 #define DFR_WO_UNROLL 4  // deal write-out unroll
 #endif
 #ifndef DFR_DV_CU
-#define DFR_DV_CU 2  // diversion rank-count loop unroll
+#define DFR_DV_CU 1  // diversion rank-count loop unroll
 #endif
 constexpr int LB_PAD = 16;  // status rows in front of pass 0's table (>= DFR_LB)
 static_assert(DFR_LB <= LB_PAD, "look-back pad");
