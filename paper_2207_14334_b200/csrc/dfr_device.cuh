@@ -23,7 +23,7 @@ constexpr int WARPS = THREADS / 32;
 #define DFR_LB_SLEEP 64  // ns of back-off when a look-back round makes no progress
 #endif
 #ifndef DFR_RANK_G
-#define DFR_RANK_G 4  // keys whose peer masks are computed together in warp_rank
+#define DFR_RANK_G 2  // keys whose peer masks are computed together in warp_rank
 #endif
 #ifndef DFR_COLD
 #define DFR_COLD __noinline__  // rare paths called from the diversion's window loop
