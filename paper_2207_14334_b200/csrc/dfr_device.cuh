@@ -34,6 +34,15 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_CLAIM_AFTER_BARRIER
 #define DFR_CLAIM_AFTER_BARRIER 1  // deal: claim the next ticket after the look-back barrier
 #endif
+// streaming TMA loads: keys are read once per pass, so they may leave L2 first
+// (DFR_TMA_EVICT_FIRST=1: L2::evict_first cache hint)
+#if DFR_TMA_EVICT_FIRST
+#define DFR_TMA_LOAD                                                                              \
+  "{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"                 \
+  " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}"
+#else
+#define DFR_TMA_LOAD "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+#endif
 #ifndef DFR_HIST_TILES
 #define DFR_HIST_TILES 8  // histogram: deal tiles counted per step of its tile loop
 #endif

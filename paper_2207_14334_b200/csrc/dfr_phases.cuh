@@ -661,13 +661,13 @@ struct Phases {
                  "r"(bytes)
                  : "memory");
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+        DFR_TMA_LOAD ::"r"(
             smem_u32(kb)),
         "l"(src), "r"(kbytes), "r"(smem_u32(bar))
         : "memory");
     if (PAIRS)
       asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          DFR_TMA_LOAD ::"r"(
               smem_u32(vb)),
           "l"(srcv), "r"(vbytes), "r"(smem_u32(bar))
           : "memory");
@@ -966,13 +966,13 @@ struct Phases {
                  "r"((uint32_t)DV_WIN_BYTES)
                  : "memory");
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+        DFR_TMA_LOAD ::"r"(
             smem_u32(S.win[b])),
         "l"(xs), "r"((uint32_t)(WIN * sizeof(K))), "r"(smem_u32(S.bar + b))
         : "memory");
     if (PAIRS)
       asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          DFR_TMA_LOAD ::"r"(
               smem_u32(S.win[b] + WIN * sizeof(K))),
           "l"(xv), "r"((uint32_t)(WIN * 4)), "r"(smem_u32(S.bar + b))
           : "memory");
