@@ -64,7 +64,7 @@ constexpr int WO_UNROLL = DFR_WO_UNROLL, DV_CU = DFR_DV_CU;
 constexpr int KPT = 16;                  // keys per thread per tile
 constexpr int TILE = THREADS * KPT;      // 4096 keys per tile (hist / deal)
 #ifndef DFR_WIN
-#define DFR_WIN 1024
+#define DFR_WIN 1280
 #endif
 constexpr int WIN = DFR_WIN;             // diversion window (keys) per CTA
 constexpr int MID_CAP = 4096;            // C: buckets N_d < s <= C finish on-chip

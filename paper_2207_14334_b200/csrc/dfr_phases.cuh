@@ -1113,9 +1113,9 @@ struct Phases {
     // ---- B: bounds, composites of owned small-bucket keys, large starts
     const uint32_t le = 0xffffffffu >> (31 - lane);
     uint32_t info[DKPT];      // bs | size << 12 | rank << 24, or DV_NONE
-    uint32_t mev[DKPT / 2];   // the composites of the lane's positions, two per word
+    uint32_t mev[(DKPT + 1) / 2];  // the composites of the lane's positions, two per word
 #pragma unroll
-    for (int m = 0; m < DKPT / 2; ++m) mev[m] = 0;
+    for (int m = 0; m < (DKPT + 1) / 2; ++m) mev[m] = 0;
     uint32_t lg = 0;
     if (nd <= 64) {
       // first start after each step (backward carry), seeded by the next warp
