@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(THREADS, 4) k_mid_s(const __grid_constant__ Pa
 // once).  Cooperative launch: every CTA is resident, levels are separated by
 // grid-wide barriers, and the loop ends on the device when the queue is empty.
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(THREADS) k_levels(const __grid_constant__ Params<K> P) {
+__global__ void __launch_bounds__(THREADS, 4) k_levels(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
   cg::grid_group grid = cg::this_grid();
   using Ph = Phases<K, PAIRS>;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(THREADS) k_levels(const __grid_constant__ Para
     grid.sync();
     for (int j = 0; j < MAX_PASSES; ++j) {
       if ((uint32_t)j >= *(volatile uint32_t*)&P.ctl->max_p) break;
-      Ph::template scatter<THREADS>(P, j, sm);
+      Ph::template scatter<THREADS, false, true>(P, j, sm);
       grid.sync();
     }
     Ph::template divert<THREADS>(P, sm);
@@ -502,6 +502,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
     pe.begin(DFR_PHASE_LEVELS);
     // level 1 through the stand-alone kernels (large recursions: c3, c4,
     // c5-low20 put most of their keys there), levels 2.. in k_levels
+#if DFR_LEVEL1_CHAIN
     launch_pdl(k_lplan<K, PAIRS>, 1, THREADS, 64, st, P);
     launch_pdl(k_hist<K, PAIRS>, g_hist, THREADS, Ph::SMEM_HIST, st, P);
     launch_pdl(k_plan2<K, PAIRS>, 4 * sms, THREADS, 64, st, P);  // one block per segment
@@ -509,6 +510,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
       launch_pdl(k_scatter<K, PAIRS>, g_sc, Ph::SC_NT, Ph::SMEM_SCATTER_P, st, P, j);
     launch_pdl(k_divert<K, PAIRS>, g_dv, Ph::DV_NT, Ph::SMEM_DIVERT, st, P);
     g_launches += 4 + MAX_PASSES;
+#endif
     void* args[] = {&P};
     const int g_lv = sms * std::max(1, dv.occ_levels);
     cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_levels<K, PAIRS>, g_lv, THREADS,

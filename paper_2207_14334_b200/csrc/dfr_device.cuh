@@ -43,6 +43,9 @@ constexpr int WARPS = THREADS / 32;
 #else
 #define DFR_TMA_LOAD "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
 #endif
+#ifndef DFR_LEVEL1_CHAIN
+#define DFR_LEVEL1_CHAIN 1  // recursion level 1 through the stand-alone kernels (else in k_levels)
+#endif
 #ifndef DFR_HIST_TILES
 #define DFR_HIST_TILES 8  // histogram: deal tiles counted per step of its tile loop
 #endif

@@ -55,8 +55,9 @@ struct Phases {
   static constexpr size_t SMEM_MID = smem_mid<MID_CAP>();
   static constexpr size_t SMEM_MID_S = smem_mid<MID_CAP_S>();
   static constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
-  static constexpr size_t SMEM_LEVEL =
-      cmax(cmax(SMEM_HIST, SMEM_SCATTER), cmax(SMEM_DIVERT, SMEM_MID));
+  // k_levels: hist, the permutation deal and the diversion (mid buckets run
+  // in k_mid / k_mid_s)
+  static constexpr size_t SMEM_LEVEL = cmax(cmax(SMEM_HIST, SMEM_SCATTER_P), SMEM_DIVERT);
 
   // ---------------------------------------------------------------- plan
   // ONE block: take the queued segments of the next level, compute p, low,
