@@ -72,7 +72,7 @@ constexpr int TILE = THREADS * KPT;      // 4096 keys per tile (hist / deal)
 constexpr int WIN = DFR_WIN;             // diversion window (keys) per CTA
 constexpr int MID_CAP = 4096;            // C: buckets N_d < s <= C finish on-chip
 #ifndef DFR_SMALL_N
-#define DFR_SMALL_N (1 << 18)
+#define DFR_SMALL_N (1 << 21)
 #endif
 constexpr int SMALL_N = DFR_SMALL_N;     // inputs up to this size: all levels in k_levels
 constexpr int MID_CAP_S = 1024;          // buckets up to this size: the 4-CTA/SM mid kernel

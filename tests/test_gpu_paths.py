@@ -1,5 +1,5 @@
 """GPU parity on the boundaries between the sort's execution paths (DESIGN.md
-§7): the small-input cooperative path (n <= 2^18) vs the stand-alone kernels,
+§7): the small-input cooperative path (n <= 2^21) vs the stand-alone kernels,
 mid buckets around the 1024-key (k_mid_s) and 4096-key (k_mid) capacities and
 just above them (global queue), recursion levels whose passes reach digit 0
 (SEG_SORTED), and several sorts queued back to back on one stream (programmatic
@@ -14,7 +14,7 @@ from gpu_util import gpu_sort, to_dev, to_host
 
 pytestmark = pytest.mark.gpu
 
-SMALL_N = 1 << 18
+SMALL_N = 1 << 21  # DFR_SMALL_N (dfr_device.cuh)
 
 
 @pytest.fixture(scope="module", autouse=True)
