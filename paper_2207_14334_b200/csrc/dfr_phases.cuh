@@ -909,6 +909,7 @@ struct Phases {
   struct Compo {
     K mask;        // remaining bits
     int sh, sl;    // (rem >> sh) << sl
+    int sh16;      // diversion, lossy: the top 16 remaining bits are rem >> sh16
     uint32_t im;   // index mask (exact mode)
     bool exact;
     __device__ __forceinline__ void init(int R, int nd) {
@@ -916,16 +917,23 @@ struct Phases {
       mask = R ? (K)(~K(0) >> (8 * sizeof(K) - R)) : K(0);
       exact = R + idxb <= 14;
       sh = exact ? 0 : R - 14;
+      sh16 = exact ? 0 : R - 16;  // R is a multiple of 8, so lossy means R >= 16
       sl = exact ? idxb : 0;
       im = exact ? 0xffu : 0u;
     }
     __device__ __forceinline__ uint16_t operator()(K k, uint32_t idx) const {
       return (uint16_t)(H_BASE + (((uint32_t)((k & mask) >> sh) << sl) | (idx & im)));
     }
-    // LOSSY: top 14 of the R remaining bits; exact: (rem << idxb) | idx
+    // LOSSY: the top 16 of the R remaining bits scaled onto the 61440 normal
+    // fp16 values of both signs, in order (negatives for the lower half:
+    // -0x7BFF .. -0x0400, then +0x0400 .. +0x7BFF): ties 3.7x rarer than with
+    // 14 bits; exact: (rem << idxb) | idx
     template <bool LOSSY>
     __device__ __forceinline__ uint16_t get(K k, uint32_t idx) const {
-      if (LOSSY) return (uint16_t)(H_BASE + ((uint32_t)(k >> sh) & 0x3fffu));
+      if (LOSSY) {
+        const uint32_t v = (((uint32_t)(k >> sh16) & 0xffffu) * 61440u) >> 16;
+        return (uint16_t)(v < 30720u ? (0x8000u | (0x0400u + 30719u - v)) : (0x0400u + v - 30720u));
+      }
       return (uint16_t)(H_BASE + (((uint32_t)(k & mask) << sl) | idx));
     }
   };
