@@ -890,7 +890,7 @@ struct Phases {
   static constexpr uint32_t DV_HOLE = 0xffffu;  // order slot not filled (window positions < WIN)
 #ifndef DFR_DV_NT
 #define DFR_DV_NT 128
-#define DFR_DV_MINB 9
+#define DFR_DV_MINB 8
 #endif
   static constexpr int DV_NT = DFR_DV_NT;     // threads of the stand-alone divert kernel
   static constexpr size_t DV_WIN_BYTES = WIN * sizeof(K) + (PAIRS ? WIN * 4 : 0);
