@@ -1083,6 +1083,7 @@ struct Phases {
     constexpr uint32_t KB = sizeof(K);
     constexpr int NONE_LO = -(1 << 20), NONE_HI = 1 << 20;
     static_assert(DKPT >= 2, "two edge words per warp");
+    static_assert(WIN % NW == 0 && WPW % 32 == 0, "each warp holds whole 32-position steps");
     const int CH = (int)P.chunk;
     const int nd = (int)P.n_d;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
