@@ -56,7 +56,7 @@ constexpr int WARPS = THREADS / 32;
 #define DFR_LB 8  // look-back predecessors loaded per round trip
 #endif
 #ifndef DFR_WO_UNROLL
-#define DFR_WO_UNROLL 4  // deal write-out unroll
+#define DFR_WO_UNROLL 6  // deal write-out unroll
 #endif
 #ifndef DFR_DV_CU
 #define DFR_DV_CU 1  // diversion rank-count loop unroll
