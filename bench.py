@@ -55,9 +55,11 @@ def parse():
     ap.add_argument("--quick", action="store_true", help="skip e2e and cpu_baseline (for ncu runs)")
     ap.add_argument("--fused", action="store_true",
                     help="dfr_config.fused_last_pass = 1 (fused last deal + diversion, DESIGN.md §8.1)")
-    ap.add_argument("--phase-events", default="all", choices=["all", "deal", "none"],
-                    help="phases timed with CUDA events inside the timed region (events between "
-                         "kernels stop programmatic dependent launch from overlapping them)")
+    ap.add_argument("--phase-events", default="none", choices=["all", "deal", "none"],
+                    help="phases timed with CUDA events inside the HEADLINE timed region (events "
+                         "between kernels stop programmatic dependent launch from overlapping "
+                         "them); the per-phase times always come from a separate run of K steps")
+    ap.add_argument("--no-cold", action="store_true", help="skip the cold-pool trial")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     return ap.parse_args()
 
@@ -160,7 +162,10 @@ def run_reference(args, rank, world):
     import datagen
     import oracle
     c, n, desc = workload(args.case, args.n)
-    sample = min(n, 1 << 24)
+    # the whole configured workload per step (about 8 s per 2^28-key sort on
+    # one core) unless the run asks for so many steps that it would take more
+    # than a few minutes: then the first 2^26 keys of the same input
+    sample = n if args.steps + args.warmup <= 30 else min(n, 1 << 26)
     keys, vals = datagen.make_case(args.case, n)
     keys = keys[:sample].copy()
     vals = vals[:sample].copy() if vals is not None else None
@@ -173,14 +178,17 @@ def run_reference(args, rank, world):
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = sample * args.steps / total / 1e9
-    samp = f"first {sample} keys of the {args.case} recipe per step, oracle.dfr_sort (1 thread)"
+    samp = (f"the whole {args.case} input ({n} keys)" if sample == n else
+            f"first {sample} of the {n} keys of the {args.case} input") + \
+        " per step, oracle.dfr_sort (1 thread, scratch allocation inside the timing)"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": c.key_dtype, "data": "synthetic",
             "config": config_dict(args.case, n, c, desc),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": samp},
+                             "sample": samp, "sample_n": sample, "cpu_model": cpu_model(),
+                             "host_cpus": os.cpu_count()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line, args)
 
@@ -215,35 +223,44 @@ def run_dfr(args, rank, world, local_rank):
     K, W = args.steps, args.warmup
     free = torch.cuda.mem_get_info(dev)[0]
     per = n * (kb + vb)
-    nbuf = int(min(K + W, max(2, (free - 3 * per - (4 << 30)) // per)))
+    ws = dfr.workspace_bytes(n, kb, vb)
+    nbuf = int(min(K + W, max(2, (free - 3 * per - ws - (4 << 30)) // per)))
     bufs = [pristine.clone() for _ in range(nbuf)]
     vbufs = [pristine_v.clone() for _ in range(nbuf)] if c.pairs else [None] * nbuf
     restore = nbuf < K + W  # not enough HBM for a copy per step: restore between steps
     stream = torch.cuda.current_stream()
     nph = len(dfr.PHASES)
-    timed = [args.phase_events == "all" or (args.phase_events == "deal" and name.startswith("scatter"))
-             for name in dfr.PHASES]
-    evs = [[torch.cuda.Event(enable_timing=True) if timed[e // 2] else None for e in range(2 * nph)]
-           for _ in range(K)]
-    for row in evs:  # torch creates the CUDA event lazily, on its first record
-        for e in row:
-            if e is not None:
-                e.record(stream)
+
+    def make_events(which):
+        timed = [which == "all" or (which == "deal" and name.startswith("scatter"))
+                 for name in dfr.PHASES]
+        evs = [[torch.cuda.Event(enable_timing=True) if timed[e // 2] else None
+                for e in range(2 * nph)] for _ in range(K)]
+        for row in evs:  # torch creates the CUDA event lazily, on its first record
+            for e in row:
+                if e is not None:
+                    e.record(stream)
+        return timed, evs
+
+    head_timed, head_evs = make_events(args.phase_events)
 
     def sort_step(i, ev=None):
         b = bufs[i % nbuf]
         vbuf = vbufs[i % nbuf]
         dfr.sort(b, vbuf, events=ev, fused=args.fused)
 
+    def restore_buf(i):
+        bufs[i % nbuf].copy_(pristine)
+        if c.pairs:
+            vbufs[i % nbuf].copy_(pristine_v)
+
     for i in range(W):
         if restore:
-            bufs[i % nbuf].copy_(pristine)
-            if c.pairs:
-                vbufs[i % nbuf].copy_(pristine_v)
+            restore_buf(i)
         sort_step(i)
     torch.cuda.synchronize()
 
-    # ---- timed region: exactly K steps
+    # ---- timed region: exactly K steps (no phase events unless asked for)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     step_ms = []
     l0 = dfr.launch_counter()
@@ -254,18 +271,16 @@ def run_dfr(args, rank, world, local_rank):
         if not restore:
             start.record(stream)
             for i in range(K):
-                sort_step(W + i, evs[i])
+                sort_step(W + i, head_evs[i] if args.phase_events != "none" else None)
             stop.record(stream)
             torch.cuda.synchronize()
             elapsed = start.elapsed_time(stop)
         else:  # per-step events; the restore copy is outside each step's events
             for i in range(K):
-                bufs[(W + i) % nbuf].copy_(pristine)
-                if c.pairs:
-                    vbufs[(W + i) % nbuf].copy_(pristine_v)
+                restore_buf(W + i)
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                sort_step(W + i, evs[i])
+                sort_step(W + i, head_evs[i] if args.phase_events != "none" else None)
                 b.record(stream)
                 torch.cuda.synchronize()
                 step_ms.append(a.elapsed_time(b))
@@ -274,19 +289,46 @@ def run_dfr(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     elapsed = reduce_max_ms(elapsed, world, dev)
+    last = bufs[(W + K - 1) % nbuf]
+    last_v = vbufs[(W + K - 1) % nbuf]
+    out_h = last.cpu().numpy().view(kdt)
+    out_v = last_v.cpu().numpy().view(np.uint32) if c.pairs else None
+    verified = verify_output(out_h, out_v, keys_h, vals_h, fp_in)
+    del out_h, out_v
 
-    # per-phase device times (CUDA events recorded by the library on this stream)
+    # ---- per-phase device times: a separate run of K steps with CUDA events the
+    # library records on this stream around each phase (the events stop
+    # programmatic dependent launch from overlapping the kernels, so this run
+    # is a little slower than the headline; its phases explain the headline)
+    ph_timed, ph_evs = make_events("all")
+    ph_step = []
+    for i in range(K):
+        restore_buf(i)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        sort_step(i, ph_evs[i])
+        b.record(stream)
+        ph_step.append((a, b))
+    torch.cuda.synchronize()
     phase_ms = {}
     for p, name in enumerate(dfr.PHASES):
-        if timed[p]:
-            phase_ms[name] = statistics.mean(evs[i][2 * p].elapsed_time(evs[i][2 * p + 1])
-                                             for i in range(K))
+        phase_ms[name] = statistics.mean(ph_evs[i][2 * p].elapsed_time(ph_evs[i][2 * p + 1])
+                                         for i in range(K))
+    phase_run_ms = statistics.mean(a.elapsed_time(b) for a, b in ph_step)
 
-    # verification of the last output: non-decreasing + same multiset as the input
-    last = bufs[(W + K - 1) % nbuf]
-    out_h = last.cpu().numpy().view(kdt)
-    verified = bool(datagen.is_sorted(out_h) and datagen.fingerprint(out_h) == fp_in)
-    del out_h
+    # ---- one cold-pool trial: the stream-ordered pool trimmed to zero first, so
+    # the call's cudaMallocAsync maps fresh memory (P:332 times allocation)
+    cold_ms = None
+    if not args.no_cold:
+        restore_buf(0)
+        torch.cuda.synchronize()
+        if trim_default_pool(local_rank):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            sort_step(0)
+            b.record(stream)
+            torch.cuda.synchronize()
+            cold_ms = a.elapsed_time(b)
 
     value = job_value(n, world, K, elapsed)
     ms_per_step = elapsed / K
@@ -325,12 +367,15 @@ def run_dfr(args, rank, world, local_rank):
             "config": config_dict(args.case, n, c, desc), "verified": verified,
             "roofline": roofline, "sort_roofline": sort_roof,
             "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
+            "phase_run_ms_per_step": round(phase_run_ms, 4),
+            "cold_pool_ms": round(cold_ms, 4) if cold_ms is not None else None,
+            "headline_phase_events": args.phase_events,
             "gpu_launches": int(launches), "clocks": clk.summary()}
 
     if not args.quick:
         line["e2e"] = run_e2e(args, dfr, torch, dev, keys_h, vals_h, tdt, n, kb, vb, world)
         if rank == 0 and world == 1:
-            line["cpu_baseline"] = run_cpu_baseline(args)
+            line["cpu_baseline"] = run_cpu_baseline(args, keys_h, vals_h)
     if rank == 0:
         emit(line, args)
 
@@ -390,36 +435,117 @@ def run_e2e(args, dfr, torch, dev, keys_h, vals_h, tdt, n, kb, vb, world):
     b.record(s_d2h)
     torch.cuda.synchronize()
     ms = reduce_max_ms(a.elapsed_time(b), world, dev)
-    ok = bool(datagen_sorted(ho.numpy().view(keys_h.dtype)))
+    ok = verify_output(ho.numpy().view(keys_h.dtype),
+                       hvo.numpy().view(np.uint32) if hvo is not None else None,
+                       keys_h, vals_h, datagen_fingerprint(keys_h))
     return {"value": job_value(n, world, K, ms), "unit": UNIT,
             "h2d_bytes_per_step": n * (kb + vb), "d2h_bytes_per_step": n * (kb + vb),
             "ms_per_step": ms / K, "pipelined_steps": NBUF, "verified": ok}
 
 
-def datagen_sorted(a):
+def datagen_fingerprint(a):
     import datagen
-    return datagen.is_sorted(a)
+    return datagen.fingerprint(a)
 
 
-def run_cpu_baseline(args):
+def verify_output(out_k, out_v, in_k, in_v, fp_in):
+    """The output is THE stable sort of the input: keys
+    non-decreasing with the input's multiset (two independent 64-bit hash-sum
+    fingerprints + count); pairs (values = input index, c4): the O(n)
+    certificate -- values a permutation of 0..n-1, out_key[i] == in_key[out_val[i]],
+    values strictly increasing inside runs of equal keys (stability)."""
     import datagen
+    ok = bool(datagen.is_sorted(out_k)) and datagen.fingerprint(out_k) == fp_in
+    if ok and out_v is not None:
+        n = out_k.size
+        ok = (np.array_equal(in_v, np.arange(n, dtype=in_v.dtype))
+              and bool((np.bincount(out_v, minlength=n) == 1).all())
+              and bool((in_k[out_v] == out_k).all()))
+        eq = out_k[1:] == out_k[:-1]
+        ok = ok and bool((out_v[1:][eq] > out_v[:-1][eq]).all())
+    return bool(ok)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_cpu_baseline(args, keys_h, vals_h):
+    """The oracle as it stands (1 thread, never tuned) on the FULL workload."""
     import oracle
-    c, n, _ = workload(args.case, args.n)
-    sample = min(n, 1 << 26)
-    keys, vals = datagen.make_case(args.case, n)
-    keys = keys[:sample].copy()
-    vals = vals[:sample].copy() if vals is not None else None
+    n = keys_h.size
     t0 = time.perf_counter()
-    oracle.dfr_sort(keys, vals, copy=False)
+    oracle.dfr_sort(keys_h, vals_h)  # sorts a copy; scratch allocation inside the timing
     dt = time.perf_counter() - t0
-    return {"value": sample / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first {sample} keys of the {args.case} recipe, one oracle.dfr_sort "
-                      f"call (1 thread, scratch allocation inside the timing), {dt:.1f} s",
-            "host_cpus": os.cpu_count()}
+    return {"value": n / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"the whole {args.case} input ({n} keys), one oracle.dfr_sort call "
+                      f"(1 thread, scratch allocation inside the timing), {dt:.1f} s",
+            "host_cpus": os.cpu_count(), "cpu_model": cpu_model()}
+
+
+def trim_default_pool(device):
+    """cudaMemPoolTrimTo(default pool of `device`, 0) through the CUDA runtime
+    torch loads (the library keeps freed scratch mapped by raising the pool's
+    release threshold; trimming makes the next call map it afresh)."""
+    import ctypes
+    import glob
+    import torch
+    cands = glob.glob(os.path.join(os.path.dirname(torch.__file__), "lib", "libcudart.so*"))
+    cands += glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_runtime",
+                                    "lib", "libcudart.so*"))
+    cands += ["libcudart.so.12", "libcudart.so"]
+    for name in cands:
+        try:
+            rt = ctypes.CDLL(name)
+            pool = ctypes.c_void_p()
+            if rt.cudaDeviceGetDefaultMemPool(ctypes.byref(pool), int(device)) != 0:
+                continue
+            return rt.cudaMemPoolTrimTo(pool, ctypes.c_size_t(0)) == 0
+        except OSError:
+            continue
+    return False
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` without a torchrun environment: re-exec this
+    script under torch.distributed.run with N ranks on this node (127.0.0.1),
+    so that a plain invocation measures N replicas as the driver's does."""
+    import socket
+    import subprocess
+    n = args.gpus
+    try:
+        import torch
+        have = torch.cuda.device_count()
+        if args.impl == "dfr" and have and have < n:
+            print(f"bench.py: --gpus {n} but only {have} CUDA devices; running {have}",
+                  file=sys.stderr)
+            n = have
+    except Exception:
+        pass
+    if n <= 1:
+        return None
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    argv = [a for a in sys.argv[1:]]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        rc = self_launch(args)
+        if rc is not None:
+            sys.exit(rc)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

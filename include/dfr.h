@@ -56,7 +56,8 @@ enum {
 
 /* Optional configuration for the _ex entry points (NULL = defaults). */
 typedef struct dfr_config {
-  uint32_t n_d;         /* diversion threshold N_d, 1 <= n_d <= 256 (default 64) */
+  uint32_t n_d;         /* diversion threshold N_d: 0 = default 64, else 8 <= n_d <= 256
+                           (other values: DFR_ERR_INVALID) */
   uint32_t skip_trivial_passes; /* 1 (default): skip a pass whose digit histogram has
                                    one non-empty bin — the identity permutation
                                    ("skipping unneeded passes"); 0: run every

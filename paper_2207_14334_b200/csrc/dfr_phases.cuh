@@ -24,6 +24,17 @@
 
 namespace dfr {
 
+// A device queue/stack capacity was exceeded.  The capacities are sized so
+// that this cannot happen; the flag is reported in dfr_stats and
+// a DFR_DEBUG build traps at once.
+__device__ __forceinline__ void flag_overflow(Ctl* c, uint32_t bit) {
+  atomicOr(&c->overflow, bit);
+#ifdef DFR_DEBUG
+  printf("dfr: device queue overflow (flag %u)\n", bit);
+  __trap();
+#endif
+}
+
 template <class K, bool PAIRS>
 struct Phases {
   using V = uint32_t;
@@ -34,7 +45,7 @@ struct Phases {
   // ------------------------------------------------------------ smem sizes
   static constexpr size_t SMEM_HIST = WARPS * MAX_PASSES * 256 * 4 + 64;
   // The deal kernel runs SC_NT threads per CTA over tiles of TILE keys
-  // (3 CTAs/SM: 24 warps hide the look-back and load latencies best)
+  // (4 CTAs/SM with the permutation deal: 32 warps hide the look-back and load latencies)
   static constexpr int SC_NT = 256;
   static constexpr int SCATTER_HDR_WORDS = (SC_NT / 32 + 1) * 256 + 256 + 32;
   static constexpr size_t SMEM_SCATTER =
@@ -69,7 +80,7 @@ struct Phases {
     const uint32_t cur = 1u - c->cur;
     uint32_t nseg = c->next_count;
     if (nseg > P.max_segs) {
-      if (threadIdx.x == 0) c->overflow |= 1;
+      if (threadIdx.x == 0) flag_overflow(c, 1u);
       nseg = P.max_segs;
     }
     Seg* q = P.segq[cur];
@@ -126,7 +137,7 @@ struct Phases {
     }
     __syncthreads();
     if (row_run > P.hist_rows) {
-      if (threadIdx.x == 0) c->overflow |= 2;
+      if (threadIdx.x == 0) flag_overflow(c, 2u);
       row_run = P.hist_rows;
     }
     for (uint32_t r = 0; r < row_run; ++r) P.hist[(size_t)r * 256 + threadIdx.x] = 0;
@@ -381,7 +392,7 @@ struct Phases {
               ns.buf = s.buf;
               nq[idx] = ns;
             } else {
-              atomicOr(&c->overflow, 4u);
+              flag_overflow(c, 4u);
             }
           }
         }
@@ -674,7 +685,8 @@ struct Phases {
           : "memory");
   }
 
-  // Persistent CTA with two tile buffers.  The next tile's ticket is claimed,
+  // Persistent CTA with two tile buffers (!PERM) or one tile buffer and a
+  // position permutation (PERM, the default deal).  The next tile's ticket is claimed,
   // and its TMA load started, as soon as the current tile has published its
   // inclusive prefix: the load and the ticket round trip overlap the current
   // tile's write-out, and tickets are still claimed in (nearly) completion
@@ -789,7 +801,12 @@ struct Phases {
       }
       fence_proxy_async();  // generic smem accesses before a later TMA into this buffer
     }
-    // every claimed ticket < total was processed, so no bulk copy is in flight here
+    // every claimed ticket < total was processed, so no bulk copy is in flight
+    // here, and every thread passed its last wait before the loop's final barrier
+    if (threadIdx.x == 0) {
+      mbar_inval(&bar[0]);
+      mbar_inval(&bar[1]);
+    }
   }
 
   // ------------------------------------------------------- small sort core
@@ -832,7 +849,7 @@ struct Phases {
         m.buf = (uint8_t)s.final_buf;
         P.midq[idx] = m;
       } else {
-        atomicOr(&c->overflow, 8u);
+        flag_overflow(c, 8u);
       }
     } else {
       const uint32_t idx = atomicAdd(&c->next_count, 1u);
@@ -845,7 +862,7 @@ struct Phases {
         ns.buf = s.final_buf;
         P.segq[1u - c->cur][idx] = ns;
       } else {
-        atomicOr(&c->overflow, 16u);
+        flag_overflow(c, 16u);
       }
     }
   }
@@ -865,8 +882,8 @@ struct Phases {
 
   // Diversion scan of one level (Alg. 4 l.7-14).  A CTA owns the buckets that
   // START in its chunk of CH = WIN - VEC - N_d keys; it holds one window of
-  // WIN keys (16-byte aligned start <= chunk start - 1; TMA bulk copies,
-  // double-buffered one window ahead) so that every owned bucket of <= N_d
+  // WIN keys (16-byte aligned start <= chunk start - 1; one TMA bulk copy into
+  // a single window buffer, refilled after each window) so that every owned bucket of <= N_d
   // keys lies inside the window.  Those are sorted on-chip into the caller's
   // buffer in the stable (insertion-sort) order; larger buckets are
   // queued (Alg. 4 l.11).
@@ -883,7 +900,8 @@ struct Phases {
   //      tie -> that bucket is re-ranked exactly on the full keys by a warp
   //   E  coalesced write of every owned slot: out[j] = window[order[j]]
   // The composite is exact — (remaining bits, index in bucket) — when the R
-  // remaining bits fit 14 - idx bits; otherwise it is the top 14 remaining bits.
+  // remaining bits fit 14 - idx bits; otherwise it is the top 16 remaining bits
+  // (scaled onto the signed normal fp16 values, Compo::get<true>).
   static constexpr uint16_t H_INF = 0x7c00;   // +inf: never below a composite
   static constexpr uint16_t H_BASE = 0x0400;  // smallest positive normal fp16
   static constexpr uint32_t DV_NONE = 0xffffffffu;
@@ -917,7 +935,10 @@ struct Phases {
       mask = R ? (K)(~K(0) >> (8 * sizeof(K) - R)) : K(0);
       exact = R + idxb <= 14;
       sh = exact ? 0 : R - 14;
-      sh16 = exact ? 0 : R - 16;  // R is a multiple of 8, so lossy means R >= 16
+      // lossy: the top 16 remaining bits; with R = 8 (possible when n_d > 64 makes the
+      // index 8 bits wide) the 16 bits reach into the bucket's shared prefix,
+      // which is constant inside a bucket, so they still order it
+      sh16 = (exact || R < 16) ? 0 : R - 16;
       sl = exact ? idxb : 0;
       im = exact ? 0xffu : 0u;
     }
@@ -1264,7 +1285,7 @@ struct Phases {
     DivertSmem S;
     char* base = reinterpret_cast<char*>(sm);
     S.win[0] = base;
-    S.win[1] = base;  // one window buffer: 10 CTAs/SM hide its refill
+    S.win[1] = base;  // one window buffer: 8 CTAs/SM (DFR_DV_MINB) hide its refill
     S.cmp = reinterpret_cast<uint16_t*>(base + DV_WIN_BYTES);
     S.order = S.cmp + DV_CMP;
     uint32_t* bm0 = reinterpret_cast<uint32_t*>(S.order + WIN);
@@ -1350,6 +1371,12 @@ struct Phases {
       // divert_window ends on a barrier: window buffer, composites and order free
       if (threadIdx.x == 0) divert_prefetch(P, q, nseg, total, ch + gridDim.x, S, 0);
       __syncthreads();  // the next window's segment / tma flag visible
+    }
+    // no copy in flight (the last prefetch found ch >= total); the shared
+    // memory is reused by the next phase of k_levels
+    if (threadIdx.x == 0) {
+      mbar_inval(S.bar);
+      mbar_inval(S.bar + 1);
     }
   }
 
@@ -1830,7 +1857,7 @@ struct Phases {
               if (sz < 512)
                 stack[sz] = make_uint2((uint32_t)bs | ((uint32_t)(bend - bs) << 16), (uint32_t)low);
               else
-                atomicOr(&c->overflow, 32u);
+                flag_overflow(c, 32u);
             }
           }
         }

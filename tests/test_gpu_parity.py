@@ -179,8 +179,8 @@ def test_stream_and_repeat():
 
 def test_divert_tie_fallback():
     """u64 buckets whose keys share the top 24 of their remaining 40 bits and
-    differ only below: the 32-bit rank composite ties and the exact re-sort of
-    the diversion must restore the order."""
+    differ only below: the 16-bit lossy rank composites tie, and the exact
+    re-rank of the diversion (full keys, index tie-break) must restore the order."""
     rng = np.random.default_rng(5)
     n = 300000
     prefix = rng.integers(0, 6000, n, dtype=np.uint64) << np.uint64(40)      # ~50 per bucket

@@ -251,3 +251,32 @@ def test_level0_structure_uniform():
     b = oracle.level_buckets(g, p, 64, 4096)
     assert b["small"] + b["mid"] + b["large"] == b["buckets"] <= 1 << 16
     assert b["large"] == 0
+
+
+def test_level_buckets_constructed_sizes():
+    """oracle_level_buckets_u64 pinned on buckets of constructed sizes around
+    both thresholds (Alg. 4 l.8-9; reading E2: size <= N_d is small,
+    S:293/S:304; <= C goes on-chip): a '<' vs '<=' slip at N_d = 64 or at
+    C = 4096, or a prefix of the wrong width, changes one of the counts."""
+    sizes = [1, 64, 65, 3, 4096, 4097, 100, 2]
+    rng = np.random.default_rng(11)
+    for p in (1, 3, 8):
+        shift = 8 * (8 - p)
+        parts = []
+        for b, s in enumerate(sizes):
+            pre = np.uint64(b + 1) << np.uint64(shift) if shift < 64 else np.uint64(0)
+            if p == 8:  # the whole key is the prefix: a bucket is a run of equal keys
+                low = np.full(s, b + 1, np.uint64)
+            else:       # random bits below the prefix, the prefix itself constant
+                low = rng.integers(0, 1 << min(shift, 62), s, dtype=np.uint64)
+            parts.append(pre | low if p < 8 else low)
+        g = np.concatenate(parts)
+        b = oracle.level_buckets(g, p, 64, 4096)
+        assert b == {"buckets": 8, "small": 4, "mid": 3, "large": 1,
+                     "mid_records": 65 + 4096 + 100, "large_records": 4097}, (p, b)
+    # N_d and C move the boundaries by exactly one record
+    g = np.concatenate([np.full(s, i, np.uint64) for i, s in enumerate(sizes)])
+    assert oracle.level_buckets(g, 8, 65, 4097)["small"] == 5
+    assert oracle.level_buckets(g, 8, 65, 4097)["large"] == 0
+    assert oracle.level_buckets(g, 8, 63, 4095)["small"] == 3
+    assert oracle.level_buckets(g, 8, 63, 4095)["large"] == 2
