@@ -53,8 +53,9 @@ def parse():
     ap.add_argument("--case", default="c5-uniform", help="datagen case (default: the headline)")
     ap.add_argument("--n", type=int, default=None, help="override the case size")
     ap.add_argument("--quick", action="store_true", help="skip e2e and cpu_baseline (for ncu runs)")
-    ap.add_argument("--fused", action="store_true",
-                    help="dfr_config.fused_last_pass = 1 (fused last deal + diversion, DESIGN.md §8.1)")
+    ap.add_argument("--fused", default="auto", choices=["auto", "off"],
+                    help="auto (default): the fused last deal + diversion where eligible; "
+                         "off: dfr_config.fused_last_pass = 2 (separate kernels)")
     ap.add_argument("--phase-events", default="none", choices=["all", "deal", "none"],
                     help="phases timed with CUDA events inside the HEADLINE timed region (events "
                          "between kernels stop programmatic dependent launch from overlapping "
@@ -247,7 +248,7 @@ def run_dfr(args, rank, world, local_rank):
     def sort_step(i, ev=None):
         b = bufs[i % nbuf]
         vbuf = vbufs[i % nbuf]
-        dfr.sort(b, vbuf, events=ev, fused=args.fused)
+        dfr.sort(b, vbuf, events=ev, fused=None if args.fused == "auto" else False)
 
     def restore_buf(i):
         bufs[i % nbuf].copy_(pristine)

@@ -66,14 +66,17 @@ typedef struct dfr_config {
                                 caller: events[2i] / events[2i+1] are recorded on `stream`
                                 before / after phase i (see DFR_PHASE_*); a phase that does
                                 not run records both back to back.  No synchronisation. */
-  uint32_t fused_last_pass; /* 0 (default): separate last deal + diversion kernels.
-                               1: a large top call (p = 3, keys only, n >= 2^27,
-                               n_d <= 64) runs its last deal and the diversion of the
-                               resulting buckets as ONE kernel over tiles made of whole
-                               runs of the two lower group digits (same output; the
-                               plain path is taken on the device when a run is longer
-                               than a tile).  Measured slower on B200:
-                               the diversion is ALU-bound, fusing saves only bytes. */
+  uint32_t fused_last_pass; /* 0 (default) or 1: a large keys-only top call (p = 3,
+                               n >= 2^27) runs its last deal and the diversion of the
+                               resulting buckets (Alg. 4 l.6 + l.7-14) as ONE kernel
+                               over tiles made of whole runs of the two lower group
+                               digits, through a second scratch buffer (A -> C -> B,
+                               fused B -> A), so the keys move once instead of twice.
+                               Same output; on the device it falls back to the
+                               separate deal + diversion when a run is longer than a
+                               tile (4608 keys) or a group pass was skipped.
+                               2: always the separate deal and diversion kernels.
+                               Other values: DFR_ERR_INVALID. */
 } dfr_config;
 
 /* Phases timed through dfr_config.phase_events. */

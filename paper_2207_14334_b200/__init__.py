@@ -122,11 +122,13 @@ def _dev_tensor(t, widths):
     return t
 
 
-def _cfg(n_d, skip_trivial, events=None, fused=False):
+def _cfg(n_d, skip_trivial, events=None, fused=None):
     """events: None or a sequence of 2*len(PHASES) torch.cuda.Event(enable_timing=True)
     (None entries: that phase is not timed).
-    fused=True asks for the fused last deal + diversion (dfr_config.fused_last_pass)."""
-    c = Config(int(n_d), 1 if skip_trivial else 0, None, 1 if fused else 0)
+    fused: None (default: the fused last deal + diversion where eligible, dfr.h),
+    True (same, explicit) or False (always the separate deal and diversion)."""
+    mode = 0 if fused is None else (1 if fused else 2)
+    c = Config(int(n_d), 1 if skip_trivial else 0, None, mode)
     if events is not None:
         arr = (ctypes.c_void_p * len(events))(*[int(e.cuda_event) if e is not None else 0
                                                   for e in events])
@@ -140,7 +142,7 @@ def launch_counter() -> int:
 
 
 def sort_u32(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, events=None,
-             fused=False):
+             fused=None):
     """In-place ascending sort of a contiguous CUDA tensor of 32-bit keys (bit
     patterns read as uint32)."""
     _dev_tensor(keys, (4,))
@@ -153,7 +155,7 @@ def sort_u32(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, event
 
 
 def sort_u64(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, events=None,
-             fused=False):
+             fused=None):
     """In-place ascending sort of a contiguous CUDA tensor of 64-bit keys (bit
     patterns read as uint64; int64 tensors are accepted as raw storage)."""
     _dev_tensor(keys, (8,))
@@ -166,7 +168,7 @@ def sort_u64(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, event
 
 
 def sort_pairs_u32(keys, vals, *, n_d=64, skip_trivial=True, stream=None, stats=False,
-                   events=None, fused=False):
+                   events=None, fused=None):
     """Stable in-place sort of (uint32 key, uint32 value) pairs held in two
     contiguous CUDA tensors of equal length."""
     _dev_tensor(keys, (4,))

@@ -41,9 +41,11 @@ __global__ void __launch_bounds__(THREADS) k_init(const __grid_constant__ Params
     s.start = 0;
     s.len = n;
     s.hi = P.D - 1;
-    s.buf = P.fuse ? 1u : 0u;  // fused level 0: the histogram kernel copies A to B first
+    s.buf = 0;
     P.segq[1][0] = s;
   }
+  if (P.J)  // the fused level's (top digit, chain) histogram, counted by k_hist
+    for (uint32_t x = threadIdx.x; x < 4096u; x += blockDim.x) P.J[x] = 0;
   if (!plan_now) return;  // small inputs: k_levels plans level 0 itself
   __syncthreads();
   Phases<K, PAIRS>::plan(P, sm);
@@ -117,10 +119,10 @@ __global__ void __launch_bounds__(Phases<K, PAIRS>::SC_NT, 4) k_scatter(const __
 
 // the middle pass of a fused level 0: the deal plus the joint histogram
 template <class K>
-__global__ void __launch_bounds__(Phases<K, false>::SC_NT, 3) k_scatter_fh(const __grid_constant__ Params<K> P, int j) {
+__global__ void __launch_bounds__(Phases<K, false>::SC_NT, 4) k_scatter_fh(const __grid_constant__ Params<K> P, int j) {
   extern __shared__ __align__(16) uint32_t sm[];
   pdl_enter();
-  Phases<K, false>::template scatter<Phases<K, false>::SC_NT, true>(P, j, sm);
+  Phases<K, false>::template scatter<Phases<K, false>::SC_NT, true, true>(P, j, sm);
 }
 
 template <class K, bool PAIRS>
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(1024) k_fplan(const __grid_constant__ Params<K
 }
 
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(Phases<K, PAIRS>::FNT, 2) k_fused(const __grid_constant__ Params<K> P) {
+__global__ void __launch_bounds__(Phases<K, PAIRS>::FNT, 3) k_fused(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
   pdl_enter();
   Phases<K, PAIRS>::fused(P, sm);
@@ -286,7 +288,7 @@ static cudaError_t get_dev(Dev& out) {
     setup((const void*)k_plan2<K, PAIRS>, 64, &d.occ_mid);
     if (err == cudaSuccess && !PAIRS)
       err = cudaFuncSetAttribute((const void*)k_scatter_fh<K>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_SCATTER);
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_SCATTER_P);
     if (err == cudaSuccess) {  // the deal (one tile buffer + permutation)
       err = cudaFuncSetAttribute((const void*)k_scatter<K, PAIRS>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_SCATTER_P);
@@ -321,7 +323,7 @@ static cudaError_t get_dev(Dev& out) {
 static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct Layout {
-  size_t b_keys, b_vals, ctl, segq0, segq1, midq, hist, status, fh, ftiles, total;
+  size_t b_keys, b_vals, c_keys, ctl, segq0, segq1, midq, hist, status, fh, ftiles, fj, total;
   size_t max_segs, mid_cap, hist_rows, tiles_max;
 };
 
@@ -334,6 +336,7 @@ static Layout make_layout(size_t n, int kb, int vb, uint32_t n_d, int min_passes
   L.hist_rows = MAX_PASSES + L.max_segs;
   for (uint64_t cap = (uint64_t)n_d << 8; cap < n; cap <<= 8) L.hist_rows += n / (cap + 1) + 1;
   L.tiles_max = 2 * (n / TILE) + L.max_segs + 2;
+  if (fuse && L.tiles_max < 65536) L.tiles_max = 65536;  // the fused pass: one tile per s-run
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -342,6 +345,7 @@ static Layout make_layout(size_t n, int kb, int vb, uint32_t n_d, int min_passes
   };
   L.b_keys = take(n * kb);
   L.b_vals = vb ? take(n * vb) : 0;
+  L.c_keys = fuse ? take(n * kb) : 0;  // fused level 0: A -> C -> B, fused pass B -> A
   L.ctl = take(sizeof(Ctl));
   L.segq0 = take(L.max_segs * sizeof(Seg));
   L.segq1 = take(L.max_segs * sizeof(Seg));
@@ -352,7 +356,8 @@ static Layout make_layout(size_t n, int kb, int vb, uint32_t n_d, int min_passes
   // LB_PAD rows in front: the look-back loads up to DFR_LB rows below tile 0
   L.status = take(((size_t)passes * L.tiles_max + LB_PAD) * 256 * 4);
   L.fh = fuse ? take(65536 * 4) : 0;      // joint histogram of the two low group digits
-  L.ftiles = fuse ? take(65536 * 8) : 0;  // run-aligned tiles of the fused pass
+  L.ftiles = fuse ? take(65536 * 16) : 0;  // run-aligned tiles of the fused pass
+  L.fj = fuse ? take(2 * 4096 * 4) : 0;     // chain histogram and bases of the fused pass
   L.total = off;
   return L;
 }
@@ -366,6 +371,8 @@ static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals,
   P.B = reinterpret_cast<K*>(ws + L.b_keys);
   P.Av = vals;
   P.Bv = pairs ? reinterpret_cast<uint32_t*>(ws + L.b_vals) : nullptr;
+  P.C = L.c_keys ? reinterpret_cast<K*>(ws + L.c_keys) : nullptr;
+  P.Cv = nullptr;
   P.ctl = reinterpret_cast<Ctl*>(ws + L.ctl);
   P.segq[0] = reinterpret_cast<Seg*>(ws + L.segq0);
   P.segq[1] = reinterpret_cast<Seg*>(ws + L.segq1);
@@ -374,7 +381,8 @@ static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals,
   P.status = reinterpret_cast<uint32_t*>(ws + L.status) + LB_PAD * 256;
   P.status_stride = L.tiles_max * 256;
   P.H = L.fh ? reinterpret_cast<uint32_t*>(ws + L.fh) : nullptr;
-  P.ftiles = L.ftiles ? reinterpret_cast<uint2*>(ws + L.ftiles) : nullptr;
+  P.ftiles = L.ftiles ? reinterpret_cast<uint4*>(ws + L.ftiles) : nullptr;
+  P.J = L.fj ? reinterpret_cast<uint32_t*>(ws + L.fj) : nullptr;
   P.max_segs = (uint32_t)L.max_segs;
   P.mid_cap = (uint32_t)L.mid_cap;
   P.hist_rows = (uint32_t)L.hist_rows;
@@ -388,11 +396,12 @@ static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals,
 static int cfg_nd(const dfr_config* cfg, uint32_t* n_d, uint32_t* skip, uint32_t* nofuse) {
   *n_d = DFR_DEFAULT_ND;
   *skip = 1;
-  *nofuse = 1;
+  *nofuse = 0;
   if (cfg) {
     *n_d = cfg->n_d ? cfg->n_d : DFR_DEFAULT_ND;
     *skip = cfg->skip_trivial_passes ? 1 : 0;
-    *nofuse = cfg->fused_last_pass ? 0 : 1;
+    if (cfg->fused_last_pass > 2) return DFR_ERR_INVALID;
+    *nofuse = cfg->fused_last_pass == 2 ? 1 : 0;
   }
   if (*n_d < 8 || *n_d > (uint32_t)MAX_ND) return DFR_ERR_INVALID;
   return DFR_OK;
@@ -421,9 +430,9 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
 
   int p0 = est_top_passes(n, n_d);
   if (p0 > (int)sizeof(K)) p0 = (int)sizeof(K);
-  // fused last pass (Phases::fused): large keys-only top calls with 3 group digits
-  const bool fuse = !PAIRS && !nofuse && p0 == 3 && n_d <= 64 && n >= ((size_t)1 << 27) &&
-                    n > (size_t)MID_CAP;
+  // fused last pass (Phases::fused): large keys-only top calls with 3 group
+  // digits (s-runs of about n / 2^16 >= 2048 keys fill a tile)
+  const bool fuse = !PAIRS && !nofuse && p0 == 3 && n >= ((size_t)1 << 27);
   const Layout L = make_layout(n, sizeof(K), PAIRS ? 4 : 0, n_d, 1, fuse);
   char* ws = nullptr;
   if (cudaMallocAsync(reinterpret_cast<void**>(&ws), L.total, st) != cudaSuccess) {
@@ -489,7 +498,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
         g_launches += 2;
       }
       if (fuse && j == 1 && !PAIRS)
-        launch_pdl(k_scatter_fh<K>, g_sc, Ph::SC_NT, Ph::SMEM_SCATTER, st, P, j);
+        launch_pdl(k_scatter_fh<K>, g_sc, Ph::SC_NT, Ph::SMEM_SCATTER_P, st, P, j);
       else
         launch_pdl(k_scatter<K, PAIRS>, g_sc, Ph::SC_NT, Ph::SMEM_SCATTER_P, st, P, j);  // no-op when fused
       pe.end(DFR_PHASE_SCATTER0 + j);
@@ -654,6 +663,17 @@ int dfr_partition_pass_pairs_u32(const uint32_t* d_keys_in, const uint32_t* d_va
 }
 
 uint64_t dfr_launch_counter(void) { return dfr::g_launches.load(); }
+
+#ifdef DFR_FPROF
+int dfr_debug_fprof(uint64_t* out16) {
+  return cudaMemcpyFromSymbol(out16, dfr::g_fprof, 16 * sizeof(uint64_t)) == cudaSuccess ? 0 : -3;
+}
+#endif
+#ifdef DFR_LB_STATS
+int dfr_debug_lb_stats(uint64_t* out4) {
+  return cudaMemcpyFromSymbol(out4, dfr::g_lb_stats, 4 * sizeof(uint64_t)) == cudaSuccess ? 0 : -3;
+}
+#endif
 
 int dfr_top_passes(size_t n, int key_bytes, uint32_t n_d) {
   if (n_d == 0) n_d = DFR_DEFAULT_ND;

@@ -61,8 +61,11 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_DV_CU
 #define DFR_DV_CU 1  // diversion rank-count loop unroll
 #endif
-constexpr int LB_PAD = 16;  // status rows in front of pass 0's table (>= DFR_LB)
-static_assert(DFR_LB <= LB_PAD, "look-back pad");
+#ifndef DFR_FLB
+#define DFR_FLB 8  // fused pass: look-back predecessors loaded per round trip
+#endif
+constexpr int LB_PAD = 32;  // status rows in front of pass 0's table (>= DFR_LB, DFR_FLB)
+static_assert(DFR_LB <= LB_PAD && DFR_FLB <= LB_PAD, "look-back pad");
 constexpr int WO_UNROLL = DFR_WO_UNROLL, DV_CU = DFR_DV_CU;
 constexpr int KPT = 16;                  // keys per thread per tile
 constexpr int TILE = THREADS * KPT;      // 4096 keys per tile (hist / deal)
@@ -91,17 +94,18 @@ constexpr uint32_t SEG_SORTED = 1u << 11;      // passes reach digit 0: sorted a
 struct Seg {                    // one DFR invocation on a contiguous bucket
   uint32_t start, len;          // element range in the arrays
   int32_t hi;                   // top remaining digit; digits above are constant
-  uint32_t buf;                 // 0: data in A (caller), 1: data in B (scratch)
+  uint32_t buf;                 // buffer id holding the data: 0 = A (caller), 1 = B, 2 = C (scratch)
   uint32_t p;                   // top passes of this invocation (Alg. 4 l.4)
   int32_t low;                  // lowest digit of the group = hi - p + 1
   uint32_t tile0;               // first tile id (exclusive prefix over segments)
   uint32_t chunk0;              // first diversion chunk id
   uint32_t hist_off;            // first histogram row (one row of 256 per pass)
   uint32_t flags;               // bits 0..3: pass j skipped; SEG_* above
-  uint32_t final_buf;           // buffer holding the data after the passes
+  uint32_t final_buf;           // buffer id holding the data after the passes
   uint32_t ntiles;              // tiles of this segment
   unsigned long long diff;      // OR over the segment of (key ^ key[start])
-  uint32_t pad[2];
+  uint32_t route;               // pass j: source id bits 4j..4j+1, destination id bits 4j+2..4j+3
+  uint32_t pad;
 };
 static_assert(sizeof(Seg) == 64, "Seg layout");
 
@@ -139,6 +143,8 @@ struct Params {
   K* B;                 // scratch keys ("buffer the same size as the input")
   uint32_t* Av;         // caller values (pairs) or null
   uint32_t* Bv;         // scratch values or null
+  K* C;                 // second scratch buffer (fused level 0 only, else null)
+  uint32_t* Cv;
   Ctl* ctl;
   Seg* segq[2];
   MidE* midq;
@@ -151,11 +157,19 @@ struct Params {
   uint32_t n_d;         // diversion threshold N_d
   uint32_t chunk;       // diversion chunk = WIN - 16/sizeof(K) - n_d
   uint32_t n;           // elements of the whole array
-  uint32_t fuse;        // level 0 may fuse its last deal with the diversion (host decision)
+  uint32_t fuse;        // level 0 may fuse its last deal with the diversion (host decision; C != null)
   uint32_t* H;          // joint histogram of the group's two low digits [d_mid][d_low] (fuse)
-  uint2* ftiles;        // run-aligned tiles of the fused pass: (segment offset, length)
+  uint4* ftiles;        // run-aligned tiles of the fused pass in ticket order:
+                        // (offset in the segment, length, ticket of the previous tile of its
+                        // chain or ~0u, chain)
+  uint32_t* J;          // fused level 0: [256][16] counts of (top digit, top 4 bits of the
+                        // middle digit), then [16][256] chain bases (exclusive over chains)
   uint32_t skip_trivial;
   int D;                // digits per key
+  __device__ __forceinline__ K* kbuf(uint32_t id) const { return id == 0 ? A : (id == 1 ? B : C); }
+  __device__ __forceinline__ uint32_t* vbuf(uint32_t id) const {
+    return id == 0 ? Av : (id == 1 ? Bv : Cv);
+  }
 };
 
 // ------------------------------------------------------------------ helpers
@@ -267,12 +281,20 @@ __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+__device__ __forceinline__ void sts64(uint32_t a, unsigned long long v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
 __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
                : "memory");
 }
 
+__device__ __forceinline__ __half2 __ushort_as_half2_pair(uint32_t h) {
+  const __half x = __ushort_as_half((unsigned short)h);
+  return __halves2half2(x, x);
+}
+__device__ __forceinline__ __half2 u2h2(uint32_t v) { return *reinterpret_cast<const __half2*>(&v); }
 __device__ __forceinline__ void red_add_shared(uint32_t saddr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
 }

@@ -24,6 +24,29 @@
 
 namespace dfr {
 
+#ifdef DFR_FPROF
+// fused-pass phase profile (timing experiments only): SM cycles per phase
+// summed over CTAs (thread 0's view), [8] tiles, [9] tiles with ties
+__device__ unsigned long long g_fprof[16];
+#define FPROF_MARK(k)                          \
+  do {                                         \
+    if (threadIdx.x == 0) {                    \
+      const long long now_ = clock64();        \
+      fp_[k] += (unsigned long long)(now_ - fp_last_); \
+      fp_last_ = now_;                         \
+    }                                          \
+  } while (0)
+#else
+#define FPROF_MARK(k) \
+  do {                \
+  } while (0)
+#endif
+#ifdef DFR_LB_STATS
+// look-back statistics of the fused pass (timing experiments only):
+// [0] extra rounds (not resolved in the first), [1] rounds that slept, [2] tiles
+__device__ unsigned long long g_lb_stats[4];
+#endif
+
 // A device queue/stack capacity was exceeded.  The capacities are sized so
 // that this cannot happen; the flag is reported in dfr_stats and
 // a DFR_DEBUG build traps at once.
@@ -43,7 +66,9 @@ struct Phases {
   static constexpr int CT_BITS = 8 * sizeof(CT);
 
   // ------------------------------------------------------------ smem sizes
-  static constexpr size_t SMEM_HIST = WARPS * MAX_PASSES * 256 * 4 + 64;
+  // warp-private digit counters + the fused level's chain histogram (256 x 16)
+  static constexpr size_t SMEM_HIST = WARPS * MAX_PASSES * 256 * 4 + 4096 * 4 + 64;
+  static constexpr int F_CHAINS = 16;  // fused pass: chains = top 4 bits of the middle digit
   // The deal kernel runs SC_NT threads per CTA over tiles of TILE keys
   // (4 CTAs/SM with the permutation deal: 32 warps hide the look-back and load latencies)
   static constexpr int SC_NT = 256;
@@ -93,6 +118,7 @@ struct Phases {
         s = q[i];
         s.diff = 0;
         s.final_buf = s.buf;
+        s.route = 0;
         chunks = (s.len + P.chunk - 1) / P.chunk;
         if (s.hi < 0) {  // digits exhausted: all keys equal (Alg. 2 l.17-18)
           s.p = 0;
@@ -158,8 +184,19 @@ struct Phases {
 
   // ---------------------------------------------------------------- hist
   static __device__ void hist_flush(const Params<K>& P, Seg* q, uint32_t si, const Seg& s,
-                                    uint32_t* sh, unsigned long long diff) {
+                                    uint32_t* sh, unsigned long long diff, uint32_t* jh) {
     __syncthreads();
+    if (jh) {  // the fused level's (top digit, chain) histogram; its marginal is the top digit's
+      uint32_t m = 0;
+      for (uint32_t x = 0; x < (uint32_t)F_CHAINS; ++x) {
+        const uint32_t i = threadIdx.x * F_CHAINS + ((x + threadIdx.x) & (F_CHAINS - 1));
+        const uint32_t v = jh[i];
+        jh[i] = 0;
+        m += v;
+        if (v) atomicAdd(&P.J[i], v);
+      }
+      sh[2 * 256 + threadIdx.x] += m;  // warp 0's row of the top group digit (pass 2)
+    }
     for (uint32_t j = 0; j < s.p; ++j) {
       uint32_t v = 0;
 #pragma unroll
@@ -180,45 +217,48 @@ struct Phases {
   // warp-private sub-histograms (no cross-warp contention).  A warp whose 32
   // keys share the whole group prefix (sorted, skewed, constant inputs) adds
   // 32 once per digit; otherwise each lane adds 1 to its digit's counter.
-  template <int NP>
-  static __device__ __forceinline__ void count_key(uint32_t shw, K k, bool valid, int low) {
+  // bin of (top group digit, top 4 bits of the middle one): the fused pass's chains
+  static __device__ __forceinline__ uint32_t chain_bin(K k, int low) {
+    return digit_of(k, low + 2) * F_CHAINS + (digit_of(k, low + 1) >> 4);
+  }
+  template <int NP, bool JT>
+  static __device__ __forceinline__ void count_key(uint32_t shw, uint32_t jsh, K k, bool valid, int low) {
     const uint32_t lane = threadIdx.x & 31;
     const K pre = k >> (8 * low);
     const K pre0 = __shfl_sync(0xffffffffu, pre, 0);
     if (__all_sync(0xffffffffu, valid && pre == pre0)) {
       if (lane == 0) {
 #pragma unroll
-        for (int j = 0; j < NP; ++j) red_add_shared(shw + 4 * (j * 256 + digit_of(k, low + j)), 32u);
+        for (int j = 0; j < (JT ? NP - 1 : NP); ++j) red_add_shared(shw + 4 * (j * 256 + digit_of(k, low + j)), 32u);
+        if (JT) red_add_shared(jsh + 4 * chain_bin(k, low), 32u);
       }
     } else if (valid) {
 #pragma unroll
-      for (int j = 0; j < NP; ++j) red_add_shared(shw + 4 * (j * 256 + digit_of(k, low + j)), 1u);
+      for (int j = 0; j < (JT ? NP - 1 : NP); ++j) red_add_shared(shw + 4 * (j * 256 + digit_of(k, low + j)), 1u);
+      if (JT) red_add_shared(jsh + 4 * chain_bin(k, low), 1u);
     }
   }
 
   // one tile: diff mask + counts of the NP group digits
-  template <int NP>
-  // cp != nullptr: the tile is also copied to cp (fused level 0 starts its
-  // passes from the scratch buffer, so that the fused last pass lands in A)
+  template <int NP, bool JT = false>
   static __device__ __forceinline__ void hist_tile(const K* tp, uint32_t cnt, K kref, int low,
-                                                   uint32_t shw, unsigned long long& diff, K* cp) {
+                                                   uint32_t shw, unsigned long long& diff,
+                                                   uint32_t jsh = 0) {
     // a tile at any offset (recursion levels): warp 0 counts the < VEC head
     // keys before the 16-byte boundary, the rest takes the vector path
     const uintptr_t mis = reinterpret_cast<uintptr_t>(tp) & 15;
-    if (mis && (mis % sizeof(K)) == 0 && (!cp || (reinterpret_cast<uintptr_t>(cp) & 15) == mis)) {
+    if (mis && (mis % sizeof(K)) == 0) {
       const uint32_t h = min(cnt, (uint32_t)((16 - mis) / sizeof(K)));
       if (threadIdx.x < 32) {
         const bool ok = threadIdx.x < h;
         const K k = ok ? tp[threadIdx.x] : K(0);
-        if (cp && ok) cp[threadIdx.x] = k;
         if (ok) diff |= (unsigned long long)(k ^ kref);
-        count_key<NP>(shw, k, ok, low);
+        count_key<NP, JT>(shw, jsh, k, ok, low);
       }
       tp += h;
       cnt -= h;
-      if (cp) cp += h;
     }
-    if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0 && (reinterpret_cast<uintptr_t>(cp) & 15) == 0) {
+    if ((reinterpret_cast<uintptr_t>(tp) & 15) == 0) {
       const uint32_t nv = cnt / VEC;
       const uint4* vp = reinterpret_cast<const uint4*>(tp);
       // independent 16-byte loads in flight per thread; a full block is at
@@ -230,9 +270,6 @@ struct Phases {
         uint4 x[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) x[u] = __ldg(vp + vb + u * THREADS + threadIdx.x);
-        if (cp)
-#pragma unroll
-          for (int u = 0; u < U; ++u) reinterpret_cast<uint4*>(cp)[vb + u * THREADS + threadIdx.x] = x[u];
         // one warp vote per block: do all U*VEC*32 keys share lane 0's group
         // prefix?  OR of (k ^ k0) | (k0 ^ kref) over the segment equals the
         // OR of (k ^ kref), so the diff mask comes from the same accumulator
@@ -248,17 +285,20 @@ struct Phases {
         if (__all_sync(0xffffffffu, (acc >> (8 * low)) == K(0))) {
           if ((threadIdx.x & 31) == 0) {
 #pragma unroll
-            for (int j = 0; j < NP; ++j)
+            for (int j = 0; j < (JT ? NP - 1 : NP); ++j)
               red_add_shared(shw + 4 * (j * 256 + digit_of(k0, low + j)), 32u * U * VEC);
+            if (JT) red_add_shared(jsh + 4 * chain_bin(k0, low), 32u * U * VEC);
           }
         } else {
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const K* kk = reinterpret_cast<const K*>(&x[u]);
 #pragma unroll
-            for (int e = 0; e < VEC; ++e)
+            for (int e = 0; e < VEC; ++e) {
 #pragma unroll
-              for (int j = 0; j < NP; ++j) red_add_shared(shw + 4 * (j * 256 + digit_of(kk[e], low + j)), 1u);
+              for (int j = 0; j < (JT ? NP - 1 : NP); ++j) red_add_shared(shw + 4 * (j * 256 + digit_of(kk[e], low + j)), 1u);
+              if (JT) red_add_shared(jsh + 4 * chain_bin(kk[e], low), 1u);
+            }
           }
         }
       }
@@ -266,30 +306,27 @@ struct Phases {
         const uint32_t v = vb + threadIdx.x;
         const bool ok = v < nv;
         uint4 x = ok ? __ldg(vp + v) : make_uint4(0, 0, 0, 0);
-        if (cp && ok) reinterpret_cast<uint4*>(cp)[v] = x;
         const K* kk = reinterpret_cast<const K*>(&x);
 #pragma unroll
         for (int e = 0; e < VEC; ++e) {
           if (ok) diff |= (unsigned long long)(kk[e] ^ kref);
-          count_key<NP>(shw, kk[e], ok, low);
+          count_key<NP, JT>(shw, jsh, kk[e], ok, low);
         }
       }
       if (nv * VEC < cnt && threadIdx.x < 32) {  // < VEC leftover keys, warp 0
         const uint32_t ii = nv * VEC + threadIdx.x;
         const bool ok = ii < cnt;
         K k = ok ? tp[ii] : K(0);
-        if (cp && ok) cp[ii] = k;
         if (ok) diff |= (unsigned long long)(k ^ kref);
-        count_key<NP>(shw, k, ok, low);
+        count_key<NP, JT>(shw, jsh, k, ok, low);
       }
     } else {
       for (uint32_t ib = 0; ib < cnt; ib += THREADS) {
         const uint32_t i = ib + threadIdx.x;
         const bool ok = i < cnt;
         K k = ok ? tp[i] : K(0);
-        if (cp && ok) cp[i] = k;
         if (ok) diff |= (unsigned long long)(k ^ kref);
-        count_key<NP>(shw, k, ok, low);
+        count_key<NP, JT>(shw, jsh, k, ok, low);
       }
     }
   }
@@ -303,8 +340,9 @@ struct Phases {
     const uint32_t total = c->total_tiles, nseg = c->nseg;
     if (total == 0) return;
     Seg* q = P.segq[c->cur];
-    const bool fcopy = P.fuse && c->level == 0;
-    if (fcopy) {  // fused level 0: clear the joint histogram and the fused pass's status rows
+    if (P.fuse && c->level == 0) {
+      // fused level 0: clear the joint histogram and the fused pass's status
+      // rows beyond the deal tiles (it may have up to 65536 run-aligned tiles)
       const uint32_t gid = blockIdx.x * THREADS + threadIdx.x, gsz = gridDim.x * THREADS;
       for (uint32_t x = gid; x < 65536u; x += gsz) P.H[x] = 0;
       uint32_t* st2 = P.status + 2 * P.status_stride;
@@ -317,13 +355,18 @@ struct Phases {
     uint32_t* sh = sm;  // [WARPS][MAX_PASSES][256]
     const uint32_t shw = smem_u32(sh + (threadIdx.x >> 5) * MAX_PASSES * 256);
     for (int j = 0; j < WARPS * MAX_PASSES; ++j) sh[j * 256 + threadIdx.x] = 0;
+    // the fused level: also the (top digit, chain) histogram of the group
+    uint32_t* jh = (P.fuse && c->level == 0) ? sm + WARPS * MAX_PASSES * 256 : nullptr;
+    const uint32_t jsh = jh ? smem_u32(jh) : 0u;
+    if (jh)
+      for (uint32_t x = threadIdx.x; x < 4096u; x += THREADS) jh[x] = 0;
     uint32_t si = upper_index(nseg, t0, [&](uint32_t i) { return q[i].tile0; });
     Seg s = q[si];
     unsigned long long diff = 0;
     __syncthreads();
     for (uint32_t t = t0; t < t1; ++t) {
       while (t >= s.tile0 + s.ntiles) {  // next segment with tiles
-        hist_flush(P, q, si, s, sh, diff);
+        hist_flush(P, q, si, s, sh, diff, s.p == 3 ? jh : nullptr);
         diff = 0;
         ++si;
         s = q[si];
@@ -337,18 +380,22 @@ struct Phases {
         for (uint32_t u = 0; u < nt; ++u)
           P.status[j * P.status_stride + (size_t)(t + u) * 256 + threadIdx.x] = 0;
       t += nt - 1;
-      const K* src = (s.buf && !fcopy) ? P.B : P.A;  // fused level 0: the input is still in A
+      const K* src = P.kbuf(s.buf);
       const K kref = src[s.start];
       const K* tp = src + base;
-      K* cp = fcopy ? P.B + base : nullptr;
       switch (s.p) {
-        case 1: hist_tile<1>(tp, cnt, kref, s.low, shw, diff, cp); break;
-        case 2: hist_tile<2>(tp, cnt, kref, s.low, shw, diff, cp); break;
-        case 3: hist_tile<3>(tp, cnt, kref, s.low, shw, diff, cp); break;
-        default: hist_tile<4>(tp, cnt, kref, s.low, shw, diff, cp); break;
+        case 1: hist_tile<1>(tp, cnt, kref, s.low, shw, diff); break;
+        case 2: hist_tile<2>(tp, cnt, kref, s.low, shw, diff); break;
+        case 3:
+          if (jh)
+            hist_tile<3, true>(tp, cnt, kref, s.low, shw, diff, jsh);
+          else
+            hist_tile<3>(tp, cnt, kref, s.low, shw, diff);
+          break;
+        default: hist_tile<4>(tp, cnt, kref, s.low, shw, diff); break;
       }
     }
-    hist_flush(P, q, si, s, sh, diff);
+    hist_flush(P, q, si, s, sh, diff, s.p == 3 ? jh : nullptr);
   }
 
   // --------------------------------------------------------------- plan2
@@ -401,9 +448,22 @@ struct Phases {
       // scan (Alg. 4 l.8) is a constant key -- insertion sort and recursion
       // leave it as it is -- so the diversion only moves the segment to A
       if (executed > 0 && s.low == 0 && c->level > 0) flags |= SEG_SORTED;
+      // buffer route of the executed passes: ping-pong between the data's
+      // buffer and another one; a level 0 with the second scratch buffer runs
+      // A -> C -> B -> C, so that its third pass (the fused pass, B -> A)
+      // lands in the caller's buffer without a copy
+      const bool three = P.C != nullptr && c->level == 0;
+      uint32_t route = 0, cur = s.buf;
+      for (uint32_t j = 0; j < s.p; ++j) {
+        if ((skip >> j) & 1u) continue;
+        const uint32_t nb = three ? (cur == 2u ? 1u : 2u) : (cur == 0u ? 1u : 0u);
+        route |= (cur | nb << 2) << (4 * j);
+        cur = nb;
+      }
       if (threadIdx.x == 0) {
         q[si].flags = flags;
-        q[si].final_buf = s.buf ^ (executed & 1u);
+        q[si].route = route;
+        q[si].final_buf = cur;
         if (c->level == 0) {
           c->level0_p = s.p;
           c->level0_run = executed;
@@ -425,9 +485,11 @@ struct Phases {
     return (uint32_t)j < s.p && !((s.flags >> j) & 1u) &&
            !(s.flags & (SEG_SKIP_DIVERT | SEG_COPY | SEG_DONE));
   }
-  static __device__ __forceinline__ uint32_t src_buf(const Seg& s, int j) {
-    const uint32_t before = (uint32_t)j - __popc(s.flags & ((1u << j) - 1u));
-    return s.buf ^ (before & 1u);
+  static __device__ __forceinline__ uint32_t route_src(const Seg& s, int j) {
+    return (s.route >> (4 * j)) & 3u;
+  }
+  static __device__ __forceinline__ uint32_t route_dst(const Seg& s, int j) {
+    return (s.route >> (4 * j + 2)) & 3u;
   }
 
 
@@ -463,14 +525,16 @@ struct Phases {
     }
     __syncthreads();
     if (FUSEH) {  // joint histogram [this digit][digit below] for the fused last pass
-      const uint32_t lo0 = digit_of(sk[0], s.low), lo1 = digit_of(sk[cnt - 1], s.low);
+      const K* tk = sk + (PERM ? (sup & 0xffu) : 0u);
+      const uint32_t lo0 = digit_of(tk[0], s.low), lo1 = digit_of(tk[cnt - 1], s.low);
       if (lo0 == lo1) {  // input sorted by the digit below: the whole tile shares it
         if (threadIdx.x < 256 && tcount[threadIdx.x])
           atomicAdd(&P.H[threadIdx.x * 256 + lo0], tcount[threadIdx.x]);
-      } else {
-#pragma unroll
-        for (int jj = 0; jj < SC_KPT; ++jj)
-          if (dr[jj] < 256) atomicAdd(&P.H[dr[jj] * 256 + digit_of(key[jj], s.low)], 1u);
+      } else {  // a tile across a boundary of the digit below (one per run of it)
+        for (uint32_t i = threadIdx.x; i < cnt; i += SC_NT) {
+          const K k = tk[i];
+          atomicAdd(&P.H[digit_of(k, dg) * 256 + digit_of(k, s.low)], 1u);
+        }
       }
     }
     // publish the tile aggregate as early as possible: successors' look-backs
@@ -537,7 +601,11 @@ struct Phases {
     }
     if (dig_thread) {
       uint32_t excl = 0;
+#ifdef DFR_D_NOLB  // timing experiment only: wrong output
+      if (false) {
+#else
       if (lt > 0) {  // decoupled look-back, up to LB predecessors per round trip
+#endif
         int tt = (int)t - 1;
         while (true) {
           constexpr int LB = DFR_LB;  // predecessors per look-back round trip
@@ -618,21 +686,21 @@ struct Phases {
     const Seg& s = q[si];
     const uint32_t lt = t - s.tile0;
     if (!pass_active(s, j) || s.len - lt * TILE < (uint32_t)TILE) return;
-    const uint32_t sb = src_buf(s, j);
-    const K* src = (sb ? P.B : P.A) + s.start + lt * TILE;
-    const V* srcv = PAIRS ? (sb ? P.Bv : P.Av) + s.start + lt * TILE : nullptr;
+    const uint32_t sb = route_src(s, j);
+    const K* src = P.kbuf(sb) + s.start + lt * TILE;
+    const V* srcv = PAIRS ? P.vbuf(sb) + s.start + lt * TILE : nullptr;
     const bool aligned = !(reinterpret_cast<uintptr_t>(src) & 15) &&
                          !(PAIRS && (reinterpret_cast<uintptr_t>(srcv) & 15));
     if (SUP) ti[3] = 0;
     if (aligned) {
     } else if (SUP) {
       const uintptr_t a = reinterpret_cast<uintptr_t>(src), a0 = a & ~(uintptr_t)15;
-      const uintptr_t k0 = reinterpret_cast<uintptr_t>(sb ? P.B : P.A);
+      const uintptr_t k0 = reinterpret_cast<uintptr_t>(P.kbuf(sb));
       if (a0 < k0 || a0 + sup_bytes(a - a0, TILE * sizeof(K)) > k0 + (uintptr_t)P.n * sizeof(K)) return;
       uint32_t off = (uint32_t)((a - a0) / sizeof(K));
       if (PAIRS) {
         const uintptr_t b = reinterpret_cast<uintptr_t>(srcv), b0 = b & ~(uintptr_t)15;
-        const uintptr_t v0 = reinterpret_cast<uintptr_t>(sb ? P.Bv : P.Av);
+        const uintptr_t v0 = reinterpret_cast<uintptr_t>(P.vbuf(sb));
         if (b0 < v0 || b0 + sup_bytes(b - b0, TILE * 4) > v0 + (uintptr_t)P.n * 4) return;
         off |= (uint32_t)((b - b0) / 4) << 8;
       }
@@ -654,9 +722,9 @@ struct Phases {
     if (!ti[2]) return;
     const Seg& s = q[ti[1]];
     const uint32_t lt = ti[0] - s.tile0;
-    const uint32_t sb = src_buf(s, j);
-    const K* src = (sb ? P.B : P.A) + s.start + lt * TILE;
-    const V* srcv = PAIRS ? (sb ? P.Bv : P.Av) + s.start + lt * TILE : nullptr;
+    const uint32_t sb = route_src(s, j);
+    const K* src = P.kbuf(sb) + s.start + lt * TILE;
+    const V* srcv = PAIRS ? P.vbuf(sb) + s.start + lt * TILE : nullptr;
     uint32_t kbytes = TILE * sizeof(K), vbytes = TILE * 4;
     if (SUP && ti[3]) {
       const uint32_t koff = ti[3] & 0xffu, voff = ti[3] >> 8;
@@ -770,11 +838,11 @@ struct Phases {
       const uint32_t lt = t - s.tile0;
       const uint32_t base = s.start + lt * TILE;
       const uint32_t cnt = min((uint32_t)TILE, s.len - lt * TILE);
-      const uint32_t sb = src_buf(s, j);
-      const K* src = sb ? P.B : P.A;
-      K* dst = sb ? P.A : P.B;
-      const V* srcv = sb ? P.Bv : P.Av;
-      V* dstv = sb ? P.Av : P.Bv;
+      const uint32_t sb = route_src(s, j), db = route_dst(s, j);
+      const K* src = P.kbuf(sb);
+      K* dst = P.kbuf(db);
+      const V* srcv = P.vbuf(sb);
+      V* dstv = P.vbuf(db);
       const int dg = s.low + j;
       if (tma) {
         mbar_wait(&bar[cb], (phases >> cb) & 1u);
@@ -832,12 +900,14 @@ struct Phases {
   }
 
   // ---------------------------------------------------------------- divert
-  static __device__ void push_bucket(const Params<K>& P, const Seg& s, uint32_t gstart,
-                                     uint32_t blen) {
+  // bucket of blen keys at gstart, held in buffer `buf`, larger than N_d:
+  // recurse on the remaining digits (Alg. 4 l.11)
+  static __device__ void push_bucket(const Params<K>& P, const Seg& s, uint32_t buf,
+                                     uint32_t gstart, uint32_t blen) {
     Ctl* c = P.ctl;
     const int hn = highest_nonconst(s.diff, s.low - 1);
     if (c->level == 0) atomicAdd(&c->level0_large, 1ull);
-    if (hn < 0 && s.final_buf == 0) return;  // constant keys, already in place
+    if (hn < 0 && buf == 0) return;  // constant keys, already in place
     if (blen <= (uint32_t)MID_CAP) {
       const uint32_t idx = atomicAdd(&c->mid_count, 1u);
       atomicAdd(&c->mid_buckets, 1ull);
@@ -846,7 +916,7 @@ struct Phases {
         m.start = gstart;
         m.len = (uint16_t)blen;
         m.hi = (int8_t)hn;
-        m.buf = (uint8_t)s.final_buf;
+        m.buf = (uint8_t)buf;
         P.midq[idx] = m;
       } else {
         flag_overflow(c, 8u);
@@ -859,7 +929,7 @@ struct Phases {
         ns.start = gstart;
         ns.len = blen;
         ns.hi = hn;
-        ns.buf = s.final_buf;
+        ns.buf = buf;
         P.segq[1u - c->cur][idx] = ns;
       } else {
         flag_overflow(c, 16u);
@@ -987,8 +1057,8 @@ struct Phases {
     window_of(P, s, ch, c0, r0, off);
     const long long abs0 = (long long)s.start + r0;
     if (abs0 < 0 || abs0 + WIN > (long long)P.n) return;
-    const K* xs = (s.final_buf ? P.B : P.A) + abs0;
-    const V* xv = PAIRS ? (s.final_buf ? P.Bv : P.Av) + abs0 : nullptr;
+    const K* xs = P.kbuf(s.final_buf) + abs0;
+    const V* xv = PAIRS ? P.vbuf(s.final_buf) + abs0 : nullptr;
     if ((reinterpret_cast<uintptr_t>(xs) & 15) || (PAIRS && (reinterpret_cast<uintptr_t>(xv) & 15)))
       return;
     fence_proxy_async();
@@ -1013,7 +1083,7 @@ struct Phases {
   // the segment), queue it (Alg. 4 l.9-11)
   static __device__ DFR_COLD void divert_large(const Params<K>& P, const Seg& s, int rb,
                                                    int known, int shift) {
-    const K* xs = (s.final_buf ? P.B : P.A) + s.start;
+    const K* xs = P.kbuf(s.final_buf) + s.start;
     const K pre = xs[rb] >> shift;
     const uint32_t len = s.len;
     uint32_t lo = (uint32_t)max(known - 1, rb);  // index known to share the prefix
@@ -1036,7 +1106,7 @@ struct Phases {
       else
         lo = mid;
     }
-    push_bucket(P, s, s.start + (uint32_t)rb, hi - (uint32_t)rb);
+    push_bucket(P, s, s.final_buf, s.start + (uint32_t)rb, hi - (uint32_t)rb);
   }
 
   // exact stable ranks of the bucket [bs, be) of the window, by one warp
@@ -1325,7 +1395,7 @@ struct Phases {
           const int nt = blockDim.x;
           int r = c0 + threadIdx.x;
           K* dA = P.A + s.start;
-          const K* sB = P.B + s.start;
+          const K* sB = P.kbuf(s.final_buf) + s.start;
           for (; r + 3 * nt < c1; r += 4 * nt) {  // four loads in flight
             const K x0 = sB[r], x1 = sB[r + nt], x2 = sB[r + 2 * nt], x3 = sB[r + 3 * nt];
             dA[r] = x0;
@@ -1335,7 +1405,8 @@ struct Phases {
           }
           for (; r < c1; r += nt) dA[r] = sB[r];
           if (PAIRS)
-            for (int rv = c0 + threadIdx.x; rv < c1; rv += nt) P.Av[s.start + rv] = P.Bv[s.start + rv];
+            for (int rv = c0 + threadIdx.x; rv < c1; rv += nt)
+              P.Av[s.start + rv] = P.vbuf(s.final_buf)[s.start + rv];
         }
         __syncthreads();
         if (threadIdx.x == 0) divert_prefetch(P, q, nseg, total, ch + gridDim.x, S, 0);
@@ -1350,8 +1421,8 @@ struct Phases {
       } else {  // window at an array edge / unaligned: plain loads
         K* wk = reinterpret_cast<K*>(S.win[b]);
         V* wv = reinterpret_cast<V*>(S.win[b] + WIN * sizeof(K));
-        const K* xs = (s.final_buf ? P.B : P.A);
-        const V* xv = PAIRS ? (s.final_buf ? P.Bv : P.Av) : nullptr;
+        const K* xs = P.kbuf(s.final_buf);
+        const V* xv = PAIRS ? P.vbuf(s.final_buf) : nullptr;
         for (int i = threadIdx.x; i < WIN; i += blockDim.x) {
           const long long a = (long long)s.start + r0 + i;
           const bool ok = a >= 0 && a < (long long)P.n;
@@ -1381,47 +1452,110 @@ struct Phases {
   }
 
   // ============================================================ fused last pass
-  // Level 0 with p = 3 group digits (lo, mid, hi) on large inputs: after the
-  // passes on lo and mid the data is sorted by (mid, lo), so every run of
-  // equal (mid, lo) -- an "s-run" -- is contiguous, and the buckets of the
-  // level (Alg. 4 l.8: equal top-3-digit prefix) are exactly the keys of one
-  // s-run that share digit hi.  A tile made of one whole s-run therefore
-  // holds its buckets complete: the last deal (Alg. 4 l.6, digit hi) and the
-  // diversion of its small buckets (l.10-14) run on the tile in one kernel,
-  // and the keys leave shared memory already in their final order.  The
-  // s-runs come from the joint histogram H[mid][lo] counted during the pass
-  // on mid.  Buckets > N_d are queued for recursion (l.11) as in the
-  // diversion kernel.  The plan kernel falls back (fused_ok = 0) to the plain
-  // deal + diversion when an s-run exceeds the tile or a pass was skipped.
-  static constexpr int FNT = 384, FKPT = 12, FNW = FNT / 32;
-  static constexpr int FT_MAX = FNT * FKPT;          // 4608 keys per tile
-  static constexpr int F_CMP = FT_MAX + 3 * 256 + 64;  // composite halves
-  struct FHdr {  // words
-    static constexpr int WHIST = 0, TC = FNW * 256, LST = TC + 256, SDST = LST + 256,
-                         BST = SDST + 256, SWARP = BST + 256, MISC = SWARP + 16, WORDS = MISC + 16;
+  // Level 0 with p = 3 group digits (lo, mid, hi) on large keys-only inputs:
+  // after the passes on lo and mid the data is sorted by (mid, lo), so every
+  // run of equal (mid, lo) -- an "s-run" -- is contiguous, and the buckets of
+  // the level (Alg. 4 l.8: equal top-3-digit prefix) are exactly the keys of
+  // one s-run that share digit hi.  A tile made of one whole s-run therefore
+  // holds its buckets complete, and the last deal (Alg. 4 l.6, digit hi) and
+  // the diversion of its small buckets (l.10-14: sorted) run on the
+  // tile in one kernel: the keys are read once and written once, in their
+  // final place (the separate deal + diversion move them twice).  The s-runs
+  // come from the joint histogram H[mid][lo] counted by the deal on mid
+  // (FUSEH); the plan kernel falls back (fused_ok = 0) to the plain deal +
+  // diversion when an s-run exceeds a tile or a pass was skipped.
+  //
+  // Inside a tile the keys are split by (hi, the top FSB remaining bits): a
+  // bucket's keys fall into 2^FSB sub-buckets that are already in order, so
+  // the small sort only ranks inside a sub-bucket (mean 4 keys at 2^28 instead
+  // of 16: a quarter of the compares, and of the warp divergence).
+  // Per tile (FNT threads, up to FT_MAX keys):
+  //   1 keys -> registers (coalesced loads; the tile was prefetched into L2);
+  //     a slot in its sub-bucket by shared atomic
+  //   2 one thread per digit value: bucket start, sub-bucket starts and
+  //     composite-area bases (one packed block scan); tile aggregate published
+  //   3 keys stored grouped by sub-bucket; the 16-bit composite (the next 16
+  //     key bits) of each key of a small bucket stored in its sub-bucket's
+  //     4-aligned composite area (padded with +inf); then, one thread per
+  //     digit value, the decoupled look-back over the earlier tiles (their
+  //     aggregates were published long before) and buckets > N_d queued for
+  //     recursion (l.11)
+  //   4 slot-major: rank = number of sub-bucket keys with a smaller composite
+  //     (packed fp16x2 compares, as in the diversion); each key is written
+  //     straight to its final place (a warp's 32 keys land in a permutation
+  //     of a few consecutive sub-buckets).  The ranks of a sub-bucket of c
+  //     keys sum to c(c-1)/2 unless two composites tie (tied keys share the
+  //     lower rank); such a sub-bucket is re-ranked exactly on the full keys
+  //     by a warp and written again.
+  // Keys only: a bucket > N_d is written in slot order, which the recursion
+  // sorts; equal keys are indistinguishable.
+  static constexpr int FNT = 256, FKPT = 18, FNW = FNT / 32;
+  // the longest s-run a tile holds (FKPT keys per thread would take 4608; the
+  // shared memory of 3 CTAs/SM takes 4576 -- an s-run of 2^28 uniform keys
+  // exceeds it with probability ~1e-9, and then the plain path runs)
+  static constexpr int FT_MAX = 4576;
+  static constexpr int FSB = 2;              // sub-bucket bits below the group
+  static constexpr int FNS = 256 << FSB;     // sub-buckets per tile
+  static constexpr int F_CMP = FT_MAX + 3 * FNS + 8;  // composite halves (areas padded to 4)
+  struct FS {                                         // shared-memory layout, byte offsets
+    static constexpr int KEYS = 0;                                      // K[FT_MAX], grouped
+    static constexpr int CMP = KEYS + FT_MAX * (int)sizeof(K);          // u16[F_CMP]
+    static constexpr int POS = CMP + F_CMP * 2;                         // u16[FT_MAX]: tile position
+    static constexpr int CNT = POS + FT_MAX * 2;                         // u32[2][FNS] (two tiles)
+    static constexpr int BDESC = CNT + 2 * FNS * 4;                     // u32[FNS]
+    static constexpr int SDST = BDESC + FNS * 4;                        // int[256]
+    static constexpr int FLAG = SDST + 1024;                            // u32[FNS/32] tie flags
+    static constexpr int WARP = FLAG + FNS / 8;                         // u32[16]
+    static constexpr int MISC = WARP + 64;                              // u32[16]
+    static constexpr int BYTES = MISC + 64;
   };
-  static constexpr size_t SMEM_FUSED =
-      (size_t)FHdr::WORDS * 4 + FT_MAX * sizeof(K) + F_CMP * 2 + FT_MAX * 2;
+  static_assert(FS::CMP % 16 == 0 && FS::CNT % 16 == 0 && FS::BDESC % 16 == 0,
+                "fused smem alignment");
+  static_assert(FS::BYTES + 1024 <= 233472 / 3, "three fused CTAs per SM");
+  static_assert(FT_MAX <= FNT * FKPT && FT_MAX % 8 == 0, "fused tile");
+  static_assert(FT_MAX < (1 << 13) && F_CMP / 4 < (1 << 11), "fused bucket descriptor fields");
+  static constexpr size_t SMEM_FUSED = FS::BYTES;
 
-  // one CTA of 1024 threads: s-run offsets and the tile list from H
+  // One CTA of 1024 threads: the s-run tiles from H and their ticket order.
+  // The look-back of the fused pass runs along F_CHAINS independent chains
+  // (chain = top 4 bits of the middle digit): a tile's exclusive prefix per top
+  // digit is the sum over the earlier tiles of ITS chain plus the chain's base,
+  // the count of keys with that top digit in all earlier chains (from the
+  // (top digit, chain) histogram the histogram kernel counted).  Tickets take
+  // the chains round robin, so consecutive tickets belong to different chains
+  // and a tile's predecessor in its chain was claimed F_CHAINS tickets
+  // earlier: its inclusive prefix is nearly always published by then, and
+  // the look-back rarely waits (one chain through all 65536 tiles cannot keep
+  // up with the rate at which tiles arrive).
   static __device__ void fplan(const Params<K>& P) {
     Ctl* c = P.ctl;
     __shared__ uint32_t s_w[32], s_w2[32], s_m[32];
     const Seg s = P.segq[c->cur][0];
-    const bool eligible = P.fuse && c->level == 0 && c->nseg == 1 && s.p == 3 &&
-                          (s.flags & (0xfu | SEG_SKIP_DIVERT | SEG_COPY | SEG_DONE | SEG_SORTED)) == 0;
+    const bool eligible = P.fuse && P.C != nullptr && c->level == 0 && c->nseg == 1 && s.p == 3 &&
+                          (s.flags & (0xfu | SEG_SKIP_DIVERT | SEG_COPY | SEG_DONE | SEG_SORTED)) == 0 &&
+                          route_src(s, 2) != 0;
     if (!eligible) {
       if (threadIdx.x == 0) c->fused_ok = 0;
       return;
     }
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const uint32_t* h = P.H + 64 * t;
+    // this thread: s-runs (middle digit, low digit) = ids [64t, 64t + 64); chain = t >> 6
+    uint32_t h[64];
+    const uint4* h4 = reinterpret_cast<const uint4*>(P.H + 64 * t);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint4 x = h4[k];
+      h[4 * k] = x.x;
+      h[4 * k + 1] = x.y;
+      h[4 * k + 2] = x.z;
+      h[4 * k + 3] = x.w;
+    }
     uint32_t sum = 0, mx = 0, nz = 0;
+#pragma unroll
     for (int k = 0; k < 64; ++k) {
-      const uint32_t x = h[k];
-      sum += x;
-      mx = max(mx, x);
-      nz += x != 0;
+      sum += h[k];
+      mx = max(mx, h[k]);
+      nz += h[k] != 0;
     }
     uint32_t a = sum, b = nz;  // inclusive warp scans
 #pragma unroll
@@ -1438,23 +1572,55 @@ struct Phases {
       s_w2[w] = b;
     }
     if (lane == 0) s_m[w] = mx;
-    __syncthreads();
-    uint32_t pa = 0, pb = 0, tot = 0, ntl = 0, gmx = 0;
-    for (int e = 0; e < 32; ++e) {
-      if (e < w) {
-        pa += s_w[e];
-        pb += s_w2[e];
+    // chain bases per top digit: exclusive over the chains
+    if (t < 256) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int ch = 0; ch < F_CHAINS; ++ch) {
+        const uint32_t x = P.J[t * F_CHAINS + ch];
+        P.J[4096 + ch * 256 + t] = acc;
+        acc += x;
       }
+    }
+    __syncthreads();
+    uint32_t pa = 0, tot = 0, ntl = 0, gmx = 0;
+    for (int e = 0; e < 32; ++e) {
+      if (e < w) pa += s_w[e];
       tot += s_w[e];
       ntl += s_w2[e];
       gmx = max(gmx, s_m[e]);
     }
+    // tiles per chain (2 warps per chain) and this thread's first index in its chain
+    uint32_t nch[F_CHAINS];
+#pragma unroll
+    for (int ch = 0; ch < F_CHAINS; ++ch) nch[ch] = s_w2[2 * ch] + s_w2[2 * ch + 1];
+    const int ch = t >> 6;
+    uint32_t jb = b - nz + ((w & 1) ? s_w2[w - 1] : 0u);  // non-empty s-runs before mine in my chain
+    uint32_t nmin = nch[0];
+#pragma unroll
+    for (int e = 1; e < F_CHAINS; ++e) nmin = min(nmin, nch[e]);
+    // ticket of the j-th tile of chain ch: round robin over the chains that
+    // still have tiles (while every chain has: F_CHAINS * j + ch)
+    auto ticket = [&](uint32_t j) {
+      if (j < nmin) return F_CHAINS * j + (uint32_t)ch;
+      uint32_t p = 0;
+#pragma unroll
+      for (int e = 0; e < F_CHAINS; ++e) p += min(nch[e], j) + ((e < ch && nch[e] > j) ? 1u : 0u);
+      return p;
+    };
     const bool ok = gmx <= (uint32_t)FT_MAX && tot == s.len;
     if (ok) {
-      uint32_t pos = pa + a - sum, ti = pb + b - nz;
+      uint32_t pos = pa + a - sum;
+      uint32_t prev = jb ? ticket(jb - 1) : ~0u;
+#pragma unroll
       for (int k = 0; k < 64; ++k) {
         const uint32_t x = h[k];
-        if (x) P.ftiles[ti++] = make_uint2(pos, x);
+        if (x) {
+          const uint32_t tk = ticket(jb);
+          P.ftiles[tk] = make_uint4(pos, x, prev, (uint32_t)ch);
+          prev = tk;
+          ++jb;
+        }
         pos += x;
       }
     }
@@ -1465,202 +1631,361 @@ struct Phases {
     }
   }
 
+  // L2 prefetch of the 16-byte aligned superset of n keys at p (bulk async)
+  static __device__ __forceinline__ void prefetch_keys_l2(const K* p, uint32_t n) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p), a0 = a & ~(uintptr_t)15;
+    const uint32_t bytes = (uint32_t)(((a + (uintptr_t)n * sizeof(K) + 15) & ~(uintptr_t)15) - a0);
+    if (bytes)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(bytes) : "memory");
+  }
+
+  // exact stable re-rank of the sub-bucket [lst, lst+cb) of the grouped keys
+  // by one warp (full keys, slot as tie-break), written to out[lst + rank]
+  static __device__ DFR_COLD void fused_fix(uint32_t keys_a, uint32_t lst, uint32_t cb, K* out) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t y = lst + lane; y < lst + cb; y += 32) {
+      const K ky = ldsk<K>(keys_a + sizeof(K) * y);
+      uint32_t r = 0;
+      for (uint32_t z = lst; z < lst + cb; ++z) {
+        const K kz = ldsk<K>(keys_a + sizeof(K) * z);
+        r += (kz < ky) || (kz == ky && z < y);
+      }
+      out[lst + r] = ky;
+    }
+  }
+
+  // exclusive scan of one value per thread over FNT threads with one barrier;
+  // s_warp must not be reused before the caller's next barrier
+  static __device__ __forceinline__ uint32_t fused_scan(uint32_t v, uint32_t* s_warp) {
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    const uint4 a = *reinterpret_cast<const uint4*>(s_warp), b = *reinterpret_cast<const uint4*>(s_warp + 4);
+    const uint32_t t[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t pre = 0;
+#pragma unroll
+    for (int e = 0; e < FNW; ++e) pre += (uint32_t)e < w ? t[e] : 0u;
+    return pre + x - v;
+  }
+
+  // Compile-time geometry of the fused pass: a level-0 group of p = 3 digits
+  // ends on the top digit, so its lowest digit is D - 3.
+  static constexpr int F_LOW = (int)sizeof(K) - 3, F_DG = (int)sizeof(K) - 1;
+  static constexpr int F_SBS = 8 * F_LOW - FSB;  // sub-bucket bits (key >> F_SBS) & 3
+  static __device__ __forceinline__ uint32_t f_sub(K k) {
+    return (uint32_t)(k >> (8 * F_DG)) << FSB | ((uint32_t)(k >> F_SBS) & ((1u << FSB) - 1));
+  }
+  // 16-bit composite of the bits below the sub-bucket bits.  u64: the next 16
+  // bits scaled onto the normal fp16 values (lossy: ties are fixed up); u32:
+  // all 6 remaining bits and the slot (< 256) -- exact and unique.
+  static __device__ __forceinline__ uint32_t f_comp(K k, uint32_t slot) {
+    if constexpr (sizeof(K) == 8) {
+      // the 16 bits scaled onto the 61440 normal fp16 values of both signs, in
+      // order (negatives first: -0x7bff .. -0x0400, then 0x0400 .. 0x7bff)
+      const uint32_t v = (((uint32_t)(k >> (F_SBS - 16)) & 0xffffu) * 61440u) >> 16;
+      return v < 30720u ? (0x8000u | (0x0400u + 30719u - v)) : (0x0400u + v - 30720u);
+    } else {
+      return 0x0400u + (((uint32_t)k & 63u) << 8 | slot);
+    }
+  }
+
   static __device__ void fused(const Params<K>& P, uint32_t* sm) {
+    constexpr bool LOSSY = sizeof(K) == 8;
     Ctl* c = P.ctl;
     if (!*(volatile uint32_t*)&c->fused_ok) return;
+    const Seg sv = P.segq[c->cur][0];
     const uint32_t ntiles = c->fused_tiles;
-    const Seg s = P.segq[c->cur][0];
-    const int j = 2, dg = s.low + 2;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int nd = (int)P.n_d;
-    uint32_t* hdr = sm;
-    uint32_t* whist = hdr + FHdr::WHIST;
-    uint32_t* mywh = whist + w * 256;
-    uint32_t* tcount = hdr + FHdr::TC;
-    uint32_t* lstart = hdr + FHdr::LST;
-    int* s_dst = reinterpret_cast<int*>(hdr + FHdr::SDST);
-    uint32_t* bst = hdr + FHdr::BST;
-    uint32_t* s_warp = hdr + FHdr::SWARP;
-    uint32_t* misc = hdr + FHdr::MISC;
-    K* sk = reinterpret_cast<K*>(hdr + ((FHdr::WORDS + 3) & ~3));
-    uint16_t* cmp = reinterpret_cast<uint16_t*>(sk + FT_MAX);
-    uint16_t* order = cmp + F_CMP;
-    const uint32_t sk_a = smem_u32(sk), cmp_a = smem_u32(cmp), order_a = smem_u32(order);
-    const uint32_t tc_s = smem_u32(tcount);
+    constexpr int j = 2;
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t nd = P.n_d;
+    char* base = reinterpret_cast<char*>(sm);
+    uint32_t* bdesc = reinterpret_cast<uint32_t*>(base + FS::BDESC);
+    int* s_dst = reinterpret_cast<int*>(base + FS::SDST);
+    uint32_t* flag = reinterpret_cast<uint32_t*>(base + FS::FLAG);
+    uint32_t* s_warp = reinterpret_cast<uint32_t*>(base + FS::WARP);
+    uint32_t* misc = reinterpret_cast<uint32_t*>(base + FS::MISC);
+    const uint32_t keys_a = smem_u32(base + FS::KEYS), cmp_a = smem_u32(base + FS::CMP),
+                   cnt0_a = smem_u32(base + FS::CNT),
+                   pos_a = smem_u32(base + FS::POS);
     uint32_t* status = P.status + (size_t)j * P.status_stride;
-    const K* src = (src_buf(s, j) ? P.B : P.A) + s.start;
-    K* dst = src_buf(s, j) ? P.A : P.B;
-    Compo comp;
-    comp.init(8 * s.low, nd);
-    if (threadIdx.x < 256) bst[threadIdx.x] = P.hist[(size_t)(s.hist_off + j) * 256 + threadIdx.x];
-
-    while (true) {
-      // ---- claim, clear, load
-      if (threadIdx.x == 0) misc[0] = atomicAdd(&c->fticket, 1u);
-      for (int e = lane; e < 256; e += 32) mywh[e] = 0;
-      if (threadIdx.x < 256) tcount[threadIdx.x] = 0;
+    const K* src = P.kbuf(route_src(sv, j)) + sv.start;
+    K* const out = P.A;
+    const uint32_t d = threadIdx.x;  // phase 2, look-back: one thread per digit value
+    const uint32_t brow = P.hist[(size_t)(sv.hist_off + j) * 256 + d];  // bucket offsets of the top digit
+    const uint32_t kofs = w * 32 * FKPT + lane;  // this thread's first key of a tile
+    auto cnt_of = [&](uint32_t cb) { return reinterpret_cast<uint32_t*>(base + FS::CNT + cb * FNS * 4); };
+    K key[FKPT];
+    uint32_t ds[FKPT];  // sub-bucket | slot << 10, or ~0u
+    // keys of tile tt -> registers; sub-bucket and slot of every key (counter set cb)
+    // ... and the tile's chain link (ticket of its predecessor in the chain, or ~0u) and chain
+    auto load_keys = [&](uint32_t tt, uint32_t& prev, uint32_t& chn) -> uint32_t {
+      uint32_t ln = 0;
+      if (tt < ntiles) {
+        const uint4 td = P.ftiles[tt];
+        ln = td.y;
+        prev = td.z;
+        chn = td.w;
+        const K* p = src + td.x + kofs;
+        const int lim = (int)ln - (int)kofs;
+#pragma unroll
+        for (int m = 0; m < FKPT; ++m) key[m] = m * 32 < lim ? p[m * 32] : K(0);
+      }
+      return ln;
+    };
+    auto count_keys = [&](uint32_t ln, uint32_t cb) {
       {
-        const uint4 inf4 = make_uint4(0x7c007c00u, 0x7c007c00u, 0x7c007c00u, 0x7c007c00u);
-        for (int x = threadIdx.x; x < F_CMP / 8; x += FNT) sts128(cmp_a + 16 * x, inf4);
-      }
-      __syncthreads();
-      const uint32_t t = misc[0];
-      if (t >= ntiles) break;
-      const uint2 td = P.ftiles[t];
-      const int len = (int)td.y;
-      const K* tsrc = src + td.x;
-#pragma unroll 4
-      for (int i = threadIdx.x; i < len; i += FNT) sk[i] = tsrc[i];
-      __syncthreads();
-      // ---- deal on digit dg (as deal_tile)
-      K key[FKPT];
-      uint32_t dr[FKPT];
-#pragma unroll
-      for (int jj = 0; jj < FKPT; ++jj) {
-        const int idx = w * 32 * FKPT + jj * 32 + lane;
-        const bool ok = idx < len;
-        key[jj] = ok ? sk[idx] : K(0);
-        dr[jj] = ok ? digit_of(key[jj], dg) : 256u;
-        if (ok) red_add_shared(tc_s + 4 * dr[jj], 1u);
-      }
-      __syncthreads();
-      const uint32_t dd = threadIdx.x;
-      const bool dig = dd < 256;
-      const uint32_t cntd = dig ? tcount[dd] : 0u;
-      if (dig) st_relaxed(status + (size_t)t * 256 + dd, (t == 0 ? FLAG_INC : FLAG_AGG) | cntd);
-      warp_rank<FKPT, false>(dr, mywh);
-      uint32_t tot;
-      const uint32_t lst = block_excl_scan<FNT>(cntd, s_warp, &tot);  // syncs: ranks done
-      if (dig) {
-        lstart[dd] = lst;
-        uint32_t acc = lst;
-#pragma unroll
-        for (int e = 0; e < FNW; ++e) {
-          const uint32_t x = whist[e * 256 + dd];
-          whist[e * 256 + dd] = acc;
-          acc += x;
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int jj = 0; jj < FKPT; ++jj) {
-        const uint32_t dgt = dr[jj] & 0xffffu;
-        if (dgt < 256) sk[mywh[dgt] + (dr[jj] >> 16)] = key[jj];
-      }
-      if (dig) {
-        uint32_t excl = 0;
-        if (t > 0) {
-          int tt = (int)t - 1;
-          while (true) {
-            constexpr int LB = 8;
-            uint32_t v[LB];
-#pragma unroll
-            for (int k = 0; k < LB; ++k)
-              v[k] = (tt - k >= 0) ? ld_relaxed(status + (size_t)(tt - k) * 256 + dd) : FLAG_INC;
-            int k = 0;
-            bool done = false;
-#pragma unroll
-            for (; k < LB; ++k) {
-              if ((v[k] >> 30) == 0) break;
-              excl += v[k] & VAL_MASK;
-              if (v[k] & FLAG_INC) {
-                done = true;
-                break;
-              }
-            }
-            if (done) break;
-            tt -= k;
-          }
-          st_relaxed(status + (size_t)t * 256 + dd, FLAG_INC | (excl + cntd));
-        }
-        s_dst[dd] = (int)(s.start + bst[dd] + excl - lst);
-      }
-      __syncthreads();
-      // ---- diversion of the tile's buckets (digit runs of the reordered tile)
-      uint32_t info[FKPT];
-#pragma unroll
-      for (int m = 0; m < FKPT; ++m) {
-        const int i = threadIdx.x + FNT * m;
-        info[m] = DV_NONE;
-        if (i < len) {
-          const K k = ldsk<K>(sk_a + sizeof(K) * i);
-          const uint32_t d = digit_of(k, dg);
-          const int bs = (int)lstart[d], sz = (int)tcount[d], idx = i - bs;
-          info[m] = d | ((uint32_t)idx << 8);
-          if (sz > 1 && sz <= nd) {
-            const int pst = (bs + 3 * (int)d + 3) & ~3;
-            sts16(cmp_a + 2 * (pst + idx), comp(k, (uint32_t)idx));
-          } else if (sz > nd && idx == 0) {
-            push_bucket(P, s, (uint32_t)s_dst[d] + (uint32_t)bs, (uint32_t)sz);
-          }
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int m = 0; m < FKPT; ++m) {
-        const int i = threadIdx.x + FNT * m;
-        if (info[m] != DV_NONE) {
-          const uint32_t d = info[m] & 255u;
-          const int idx = (int)(info[m] >> 8);
-          const int bs = (int)lstart[d], sz = (int)tcount[d];
-          uint32_t rk = (uint32_t)idx;
-          if (sz > 1 && sz <= nd) {
-            const int pst = (bs + 3 * (int)d + 3) & ~3;
-            const uint32_t me = lds16(cmp_a + 2 * (pst + idx));
-            const __half2 me2 = __halves2half2(__ushort_as_half((unsigned short)me),
-                                               __ushort_as_half((unsigned short)me));
-            uint32_t pa = cmp_a + 2 * pst;
-            const uint32_t pe = pa + 8 * ((sz + 3) >> 2);
-            __half2 acc = __float2half2_rn(0.f);
-#pragma unroll 2
-            for (; pa < pe; pa += 8) {
-              const uint2 v = lds64v(pa);
-              acc = __hadd2(acc, __hlt2(*reinterpret_cast<const __half2*>(&v.x), me2));
-              acc = __hadd2(acc, __hlt2(*reinterpret_cast<const __half2*>(&v.y), me2));
-            }
-            rk = (uint32_t)__half2ushort_rz(__hadd(__low2half(acc), __high2half(acc)));
-          }
-          sts16(order_a + 2 * (bs + (int)rk), (uint32_t)i);
-          info[m] = d | ((uint32_t)idx << 8) | (rk << 21);  // idx < 2^13, rk < 2^11
-        }
-      }
-      if (!comp.exact) {  // tie check: a slot claimed by another key
-        __syncthreads();
-        uint32_t badm = 0;
+        const int lim = (int)ln - (int)kofs;
+        const uint32_t ca = cnt0_a + cb * FNS * 4;
 #pragma unroll
         for (int m = 0; m < FKPT; ++m) {
-          const int i = threadIdx.x + FNT * m;
-          if (info[m] != DV_NONE) {
-            const uint32_t d = info[m] & 255u;
-            const uint32_t bs = lstart[d];
-            badm |= (uint32_t)(lds16(order_a + 2 * (bs + (info[m] >> 21))) != (uint32_t)i) << m;
+          ds[m] = ~0u;
+          if (m * 32 < lim) {
+            const uint32_t sb = f_sub(key[m]);
+            uint32_t slot;
+            asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(slot) : "r"(ca + 4 * sb) : "memory");
+            ds[m] = sb | slot << 10;
           }
         }
-        if (__syncthreads_or(badm != 0)) {
+      }
+    };
+    // the tile aggregate of digit d, published as soon as the counts are
+    // complete; the first tile of a chain publishes its inclusive prefix
+    // (the chain's base + its count) at once
+    const uint32_t* jbase = P.J + 4096;
+    auto publish = [&](uint32_t tt, uint32_t cb, uint32_t prev, uint32_t chn) {
+      if (tt < ntiles) {
+        const uint4 c4 = reinterpret_cast<const uint4*>(cnt_of(cb))[d];
+        const uint32_t cdd = c4.x + c4.y + c4.z + c4.w;
+        st_relaxed(status + (size_t)tt * 256 + d,
+                   prev == ~0u ? (FLAG_INC | (jbase[chn * 256 + d] + cdd)) : (FLAG_AGG | cdd));
+      }
+    };
+    reinterpret_cast<uint4*>(cnt_of(0))[d] = make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(cnt_of(1))[d] = make_uint4(0, 0, 0, 0);
+    if (d < FNS / 32) flag[d] = 0;
+    // tickets are claimed one tile ahead, so that a tile's keys are in L2
+    // (bulk prefetch at its claim) by the time they are loaded
+    if (d == 0) {
+      misc[0] = atomicAdd(&c->fticket, 1u);
+      misc[1] = atomicAdd(&c->fticket, 1u);
+      misc[3] = 0;
+      if (misc[1] < ntiles) {
+        const uint4 tn = P.ftiles[misc[1]];
+        prefetch_keys_l2(src + tn.x, tn.y);
+      }
+    }
+    __syncthreads();
+    uint32_t t = misc[0], tq = misc[1], cur = 0, tprev = ~0u, tch = 0;
+#ifdef DFR_FPROF
+    unsigned long long fp_[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long fp_last_ = clock64();
+#endif
+    uint32_t len = load_keys(t, tprev, tch);
+    count_keys(len, 0);
+    __syncthreads();
+    publish(t, 0, tprev, tch);
+    while (t < ntiles) {
+      FPROF_MARK(0);  // (the previous tile's tail)
+      // ---- 2: bucket layout (thread d: digit value d and its sub-buckets)
+      static_assert(FSB == 2, "four sub-buckets per digit value");
+      const uint4 c4 = reinterpret_cast<const uint4*>(cnt_of(cur))[d];
+      const uint32_t cs[4] = {c4.x, c4.y, c4.z, c4.w};
+      const uint32_t cd = c4.x + c4.y + c4.z + c4.w;
+      const bool small = cd <= nd;
+      uint32_t padc = 0;
 #pragma unroll
-          for (int m = 0; m < FKPT; ++m) {
-            const bool b = (badm >> m) & 1u;
-            uint32_t bmk = __ballot_sync(0xffffffffu, b);
-            const uint32_t d = info[m] & 255u;
-            while (bmk) {
-              const uint32_t dl = __shfl_sync(0xffffffffu, d, __ffs(bmk) - 1);
-              bmk &= ~__ballot_sync(0xffffffffu, b && d == dl);
-              rerank_exact(sk_a, order_a, (int)lstart[dl], (int)(lstart[dl] + tcount[dl]));
-            }
-          }
+      for (int r = 0; r < 4; ++r) padc += (small && cs[r] >= 2) ? (cs[r] + 3) & ~3u : 0u;
+      const uint32_t ex = fused_scan(cd | padc << 16, s_warp);
+      const uint32_t lst = ex & 0xffffu;
+      {
+        uint32_t so = lst, co = ex >> 16;
+        uint32_t bd[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint32_t ng = (small && cs[r] >= 2) ? (cs[r] + 3) >> 2 : 0u;
+          bd[r] = (co >> 2) | ng << 11 | so << 18;
+          // the last group of the area := +inf; phase 3 overwrites its real entries
+          if (ng) sts64(cmp_a + 2 * (co + 4 * ng - 4), 0x7c007c007c007c00ull);
+          so += cs[r];
+          co += 4 * ng;
+        }
+        reinterpret_cast<uint4*>(bdesc)[d] = make_uint4(bd[0], bd[1], bd[2], bd[3]);
+      }
+      __syncthreads();
+      FPROF_MARK(1);
+      // ---- 3: keys grouped by sub-bucket, composites of small-bucket keys
+      if (d == 0) misc[3] = 0;  // the tile's tie check accumulator (read before phase 2's barrier)
+#pragma unroll
+      for (int m = 0; m < FKPT; ++m) {
+        if (ds[m] != ~0u) {
+          const uint32_t slot = ds[m] >> 10;
+          const uint32_t bd = bdesc[ds[m] & (FNS - 1)];
+          const uint32_t x = (bd >> 18) + slot;
+          if constexpr (sizeof(K) == 8)
+            sts64(keys_a + 8 * x, (unsigned long long)key[m]);
+          else
+            sts32(keys_a + 4 * x, (uint32_t)key[m]);
+          if ((bd >> 11) & 127u) sts16(cmp_a + 2 * (4 * (bd & 2047u) + slot), f_comp(key[m], slot));
         }
       }
       __syncthreads();
-      // ---- write every slot in final order
+      FPROF_MARK(2);
+      // ---- 4: slot-major rank inside each sub-bucket -> final tile position.
+      // Without ties the positions are a permutation of the slots, so the
+      // sum over the tile of (position - slot) is 0; tied keys share the lower
+      // rank, which makes it negative (checked after the write-out)
+      int dev = 0;
+      for (uint32_t x = threadIdx.x; x < len; x += FNT) {
+        const uint32_t bd = bdesc[f_sub(ldsk<K>(keys_a + sizeof(K) * x))];
+        const uint32_t ng = (bd >> 11) & 127u;
+        uint32_t pos = x;
+        if (ng) {
+          const uint32_t bl = bd >> 18;
+          const uint32_t pa = cmp_a + 8 * (bd & 2047u);
+          const uint32_t me = lds16(pa + 2 * (x - bl));
+          const __half2 me2 = __ushort_as_half2_pair(me);
+          // the first two groups (sub-buckets <= 8 keys) without a loop
+          const uint2 v0 = lds64v(pa);
+          uint2 v1 = make_uint2(0x7c007c00u, 0x7c007c00u);
+          if (ng > 1) v1 = lds64v(pa + 8);
+          __half2 acc = __hadd2(__hlt2(u2h2(v0.x), me2), __hlt2(u2h2(v0.y), me2));
+          acc = __hadd2(acc, __hlt2(u2h2(v1.x), me2));
+          acc = __hadd2(acc, __hlt2(u2h2(v1.y), me2));
+          for (uint32_t g = 2; g < ng; ++g) {  // rare: larger sub-buckets
+            const uint2 v = lds64v(pa + 8 * g);
+            acc = __hadd2(acc, __hlt2(u2h2(v.x), me2));
+            acc = __hadd2(acc, __hlt2(u2h2(v.y), me2));
+          }
+          const uint32_t rk = (uint32_t)__half2ushort_rz(__hadd(__low2half(acc), __high2half(acc)));
+          pos = bl + rk;
+          dev += (int)pos - (int)x;
+        }
+        sts16(pos_a + 2 * x, pos);
+      }
+      if (LOSSY) {
 #pragma unroll
-      for (int m = 0; m < FKPT; ++m) {
-        const int i = threadIdx.x + FNT * m;
-        if (info[m] != DV_NONE) {
-          const uint32_t srcpos = lds16(order_a + 2 * i);
-          dst[(uint32_t)s_dst[info[m] & 255u] + (uint32_t)i] = ldsk<K>(sk_a + sizeof(K) * srcpos);
+        for (int o = 16; o; o >>= 1) dev += __shfl_xor_sync(0xffffffffu, dev, o);
+        if (lane == 0 && dev) atomicAdd(reinterpret_cast<int*>(misc + 3), dev);
+      }
+      // the ticket after the next one (its keys prefetched into L2); the next
+      // tile's keys are loaded while this tile's look-back runs, and counted
+      // and its aggregate published when this tile has been written out
+      if (d == 0) {
+        const uint32_t tw = atomicAdd(&c->fticket, 1u);
+        misc[1] = tw;
+        if (tw < ntiles) {
+          const uint4 tnw = P.ftiles[tw];
+          prefetch_keys_l2(src + tnw.x, tnw.y);
         }
       }
+      __syncthreads();
+      FPROF_MARK(3);
+      const uint32_t tn = tq;
+      tq = misc[1];
+      uint32_t nprev = ~0u, nchn = 0;
+      const uint32_t lenn = load_keys(tn, nprev, nchn);
+      // ---- decoupled look-back along this tile's chain (thread d, digit d)
+      {
+        uint32_t excl;
+        if (tprev == ~0u) {
+          excl = jbase[tch * 256 + d];  // first tile of its chain: published with the counts
+        } else {
+          excl = 0;
+#ifndef DFR_F_NOLB  // (timing experiment only: wrong output)
+          uint32_t pt = tprev;
+          while (true) {
+            const uint32_t v = ld_relaxed(status + (size_t)pt * 256 + d);
+            if ((v >> 30) == 0) {  // not published yet
+#ifdef DFR_LB_STATS
+              atomicAdd(&g_lb_stats[1], 1ull);
+#endif
+              __nanosleep(DFR_LB_SLEEP);
+              continue;
+            }
+            excl += v & VAL_MASK;
+            if (v & FLAG_INC) break;
+#ifdef DFR_LB_STATS
+            atomicAdd(&g_lb_stats[0], 1ull);
+#endif
+            pt = P.ftiles[pt].z;
+          }
+#endif
+#ifdef DFR_LB_STATS
+          if (d == 0) atomicAdd(&g_lb_stats[2], 1ull);
+#endif
+          st_relaxed(status + (size_t)t * 256 + d, FLAG_INC | (excl + cd));
+        }
+        const uint32_t gstart = sv.start + brow + excl;  // global index of bucket (d, this s-run)
+        s_dst[d] = (int)(gstart - lst);
+        if (!small) push_bucket(P, sv, 0u, gstart, cd);  // written to A below (Alg. 4 l.11)
+      }
+      __syncthreads();  // s_dst complete
+      FPROF_MARK(4);
+      // ---- 5: this tile in final order (keys and positions read in slot order)
+#pragma unroll 4
+      for (uint32_t x = threadIdx.x; x < len; x += FNT) {
+        const K k = ldsk<K>(keys_a + sizeof(K) * x);
+        out[(uint32_t)s_dst[digit_of(k, F_DG)] + lds16(pos_a + 2 * x)] = k;
+      }
+      // the next tile's keys have arrived meanwhile: count them, publish its aggregate
+      count_keys(lenn, cur ^ 1u);
+      __syncthreads();
+      publish(tn, cur ^ 1u, nprev, nchn);
+      FPROF_MARK(5);
+#ifdef DFR_FPROF
+      if (threadIdx.x == 0) { fp_[8]++; fp_[9] += misc[3] != 0; }
+#endif
+      if (LOSSY && misc[3] != 0) {
+        // (rare) tied composites in this tile: a sub-bucket of c keys at bl
+        // whose positions do not sum to c*bl + c(c-1)/2 is re-ranked exactly
+        uint32_t bad = 0;
+        {
+          const uint4 b4 = reinterpret_cast<const uint4*>(bdesc)[d];
+          const uint32_t bds[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (small && cs[r] >= 2) {
+              const uint32_t bl = bds[r] >> 18;
+              uint32_t ps = 0;
+              for (uint32_t y = bl; y < bl + cs[r]; ++y) ps += lds16(pos_a + 2 * y);
+              bad |= (uint32_t)(ps != cs[r] * bl + cs[r] * (cs[r] - 1) / 2) << r;
+            }
+        }
+        {
+          if (bad) atomicOr(&flag[d >> 3], bad << (4 * (d & 7)));
+          __syncthreads();
+          const uint32_t* cntc = cnt_of(cur);
+          for (uint32_t fw = w; fw < FNS / 32; fw += FNW) {
+            uint32_t bits = flag[fw];
+            while (bits) {
+              const uint32_t sb = fw * 32 + __ffs(bits) - 1;
+              bits &= bits - 1;
+              fused_fix(keys_a, bdesc[sb] >> 18, cntc[sb], out + (uint32_t)s_dst[sb >> FSB]);
+            }
+          }
+          __syncthreads();
+          if (d < FNS / 32) flag[d] = 0;
+        }
+      }
+      // this tile's counters are read by no one any more
+      reinterpret_cast<uint4*>(cnt_of(cur))[d] = make_uint4(0, 0, 0, 0);
+      t = tn;
+      len = lenn;
+      tprev = nprev;
+      tch = nchn;
+      cur ^= 1u;
+      FPROF_MARK(6);
     }
+#ifdef DFR_FPROF
+    if (threadIdx.x == 0)
+      for (int k = 0; k < 10; ++k) atomicAdd(&g_fprof[k], fp_[k]);
+#endif
   }
 
   // ------------------------------------------------------------------ mid
@@ -1742,13 +2067,13 @@ struct Phases {
       const MidE me = P.midq[e];
       const int len = me.len;
       if (len <= len_lo || len > CAP) continue;  // the other instantiation's bucket
-      const K* X = me.buf ? P.B : P.A;
-      const V* Xv = me.buf ? P.Bv : P.Av;
+      const K* X = P.kbuf(me.buf);
+      const V* Xv = P.vbuf(me.buf);
       if (me.hi < 0) {  // digits exhausted: a constant bucket, sorted (Alg. 2 l.17-18)
         if (me.buf)  // left in the scratch buffer: copy out
           {
-            coop_copy(P.A + me.start, P.B + me.start, (uint32_t)len, threadIdx.x, THREADS);
-            if (PAIRS) coop_copy(P.Av + me.start, P.Bv + me.start, (uint32_t)len, threadIdx.x, THREADS);
+            coop_copy(P.A + me.start, X + me.start, (uint32_t)len, threadIdx.x, THREADS);
+            if (PAIRS) coop_copy(P.Av + me.start, Xv + me.start, (uint32_t)len, threadIdx.x, THREADS);
           }
         continue;
       }

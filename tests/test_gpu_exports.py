@@ -43,6 +43,10 @@ def test_u32_keys_distinct_p3(n):
     rk, _, ost = oracle.dfr_sort(k)
     assert st["level0_p"] == ost["level0_p"] == 3 and st["overflow"] == 0
     _same(gk, rk, "keys")
+    if n >= 1 << 27:  # the separate stand-alone deal + diversion as well
+        gk, _, st = gpu_sort(k, stats=True, fused=False)
+        assert st["fused"] == 0
+        _same(gk, rk, "keys (separate last pass)")
 
 
 @pytest.mark.parametrize("n", [1 << 23, (1 << 23) + 777, 1 << 27])
