@@ -10,5 +10,5 @@ for _ in range(3):
 torch.cuda.synchronize()
 out = (ctypes.c_uint64 * 4)()
 dfr.lib().dfr_debug_lb_stats(out)
-print("extra steps", out[0], "sleeps", out[1], "tiles(x3 sorts)", out[2], "steps per tile", out[0] / max(1, out[2]),
+print("extra rounds", out[0], "sleeps", out[1], "look-backs", out[2], "extra rounds per look-back", out[0] / max(1, out[2]),
       "extra rounds per tile-digit", out[0] / max(1, out[2]) / 256)
