@@ -148,6 +148,20 @@ int dfr_partition_pass_pairs_u32(const uint32_t* d_keys_in, const uint32_t* d_va
                                  uint32_t* d_keys_out, uint32_t* d_vals_out, size_t n, int d,
                                  dfr_stream_t stream);
 
+/*
+ * Monte Carlo of the Fast Radix overflow model (§3.1, P:292-306;
+ * Alg. 3): each of `trials` experiments throws n records into m
+ * buckets uniformly at random and writes its overflow against the estimated
+ * capacity ceil(n/m),  sum_i max(0, count_i - ceil(n/m)),  to d_overflow[t]
+ * (device array of `trials` uint64, caller-owned).  Random numbers: SplitMix64
+ * counter-based: trial t's stream key is mix(key + (t+1)*GAMMA) and record b
+ * goes to bucket hi32(mix(k_t + (b+1)*GAMMA)) * m >> 32 (GAMMA =
+ * 0x9E3779B97F4A7C15).  1 <= m <= 16384; trials == 0 is a no-op.
+ * Asynchronous on `stream`; DFR_ERR_INVALID for a NULL array or m out of range.
+ */
+int dfr_overflow_mc(uint64_t n, uint32_t m, uint32_t trials, uint64_t key, uint64_t* d_overflow,
+                    dfr_stream_t stream);
+
 /* Number of top passes the planner uses for n keys (Alg. 4 l.4), capped at D. */
 int dfr_top_passes(size_t n, int key_bytes, uint32_t n_d);
 

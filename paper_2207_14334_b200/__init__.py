@@ -15,7 +15,7 @@ import os
 
 __all__ = [
     "DfrError", "lib", "sort", "sort_u32", "sort_u64", "sort_pairs_u32", "histogram",
-    "partition_pass", "top_passes", "workspace_bytes", "status_string", "EXPORTS",
+    "partition_pass", "top_passes", "workspace_bytes", "status_string", "EXPORTS", "overflow_mc",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -28,6 +28,7 @@ EXPORTS = (
     "dfr_histogram_u32", "dfr_histogram_u64",
     "dfr_partition_pass_u64", "dfr_partition_pass_pairs_u32",
     "dfr_top_passes", "dfr_workspace_bytes", "dfr_launch_counter", "dfr_status_string",
+    "dfr_overflow_mc",
 )
 
 PHASES = ("hist", "plan", "scatter0", "scatter1", "scatter2", "scatter3", "divert", "levels", "mid")
@@ -83,6 +84,7 @@ def lib() -> ctypes.CDLL:
         "dfr_workspace_bytes": [sz, i32, i32],
         "dfr_status_string": [i32],
         "dfr_launch_counter": [],
+        "dfr_overflow_mc": [ctypes.c_uint64, u32, u32, ctypes.c_uint64, p, p],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -220,6 +222,16 @@ def partition_pass(keys, d: int, vals=None, *, stream=None):
         vo.data_ptr() if vo is not None else None, keys.numel(), d, _stream(stream)),
         "dfr_partition_pass_pairs_u32")
     return ko, vo
+
+
+def overflow_mc(n: int, m: int, trials: int, key: int, *, stream=None):
+    """Fast Radix overflow Monte Carlo (dfr_overflow_mc): int64 CUDA tensor of
+    the per-trial overflow sum_i max(0, count_i - ceil(n/m))."""
+    import torch
+    out = torch.empty(trials, dtype=torch.int64, device="cuda")
+    _check(lib().dfr_overflow_mc(n, m, trials, key & ((1 << 64) - 1), out.data_ptr(), _stream(stream)),
+           "dfr_overflow_mc")
+    return out
 
 
 def top_passes(n: int, key_bytes: int = 8, n_d: int = 64) -> int:

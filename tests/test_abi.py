@@ -20,7 +20,7 @@ def _declared():
 def test_library_exports_every_declared_symbol():
     L = dfr.lib()
     decl = _declared()
-    assert len(decl) == 14
+    assert len(decl) == 15
     assert sorted(dfr.EXPORTS) == decl
     for name in decl:
         assert hasattr(L, name), name
