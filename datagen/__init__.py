@@ -188,6 +188,15 @@ CASES = {
     "c5-nearly": Case("c5-nearly", "c5", 1 << 28, "u64", False, 5),
     "c5-runs": Case("c5-runs", "c5", 1 << 28, "u64", False, 5),
     "c5-low20": Case("c5-low20", "c5", 1 << 28, "u64", False, 5),
+    # the paper's own workloads: 64-bit keys at
+    # N = 256^3 .. 256^3.75, uniform (Fig. 1), wide normal
+    # (mean ~2^63, sd ~2^61; Fig. 2), narrow normal (mean ~2^32, sd
+    # ~2^30; Fig. 3); n is chosen per run (default 256^3.5 = 2^28)
+    "paper-uniform": Case("paper-uniform", "paper", 1 << 28, "u64", False, 6),
+    "paper-wide-normal": Case("paper-wide-normal", "paper", 1 << 28, "u64", False, 6),
+    "paper-narrow-normal": Case("paper-narrow-normal", "paper", 1 << 28, "u64", False, 6),
+    # 16-byte records (SPEC's key + tag): uniform u64 keys, u64 tags
+    "paper-records": Case("paper-records", "paper", 1 << 27, "u64", True, 6),
 }
 
 
@@ -212,6 +221,14 @@ def make_case(name: str, n: int | None = None):
         return few_unique_u32(n, s, 256), vals
     if name == "c4-equal":
         return const_u32(n, s), vals
+    if name == "paper-uniform":
+        return uniform_u64(n, s, "paper-uniform"), None
+    if name == "paper-wide-normal":
+        return normal_u64(n, s, 1 << 63, 2.0 ** 61, "paper-wide"), None
+    if name == "paper-narrow-normal":
+        return normal_u64(n, s, 1 << 32, 2.0 ** 30, "paper-narrow"), None
+    if name == "paper-records":
+        return uniform_u64(n, s, "paper-records"), uniform_u64(n, s, "paper-tags")
     base = uniform_u64(n, s, "base")
     if name == "c5-uniform":
         return base, None

@@ -77,6 +77,11 @@ typedef struct dfr_config {
                                tile (4608 keys) or a group pass was skipped.
                                2: always the separate deal and diversion kernels.
                                Other values: DFR_ERR_INVALID. */
+  uint32_t full_lsd;        /* 0 (default).  1: ablation (SPEC AC7): the top call
+                               runs a plain LSD radix sort over ALL D digits (p = D, no
+                               diversion, no recursion).  u32 keys and u32 pairs only
+                               (D = 4); DFR_ERR_INVALID for u64 keys.  Inputs of at most
+                               4096 keys still run the on-chip DFR. */
 } dfr_config;
 
 /* Phases timed through dfr_config.phase_events. */
@@ -118,6 +123,16 @@ int dfr_sort_u64(uint64_t* d_keys, size_t n, dfr_stream_t stream);
  */
 int dfr_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_vals, size_t n, dfr_stream_t stream);
 
+/*
+ * Stable sort of n (uint64 key, uint64 value) records held as two arrays
+ * (SoA; SPEC's 16-byte Record key + tag).  d_vals[i] moves with
+ * d_keys[i]; equal keys keep their input order.  Keys and values must
+ * not overlap; both 8-byte aligned.  The keys are sorted with their uint32
+ * input positions as the payload (the pairs path), then the values follow that
+ * permutation (a gather into scratch and a copy back).
+ */
+int dfr_sort_pairs_u64(uint64_t* d_keys, uint64_t* d_vals, size_t n, dfr_stream_t stream);
+
 /* Same as above with a configuration and optional stats (stats != NULL
  * synchronises `stream`). */
 int dfr_sort_u32_ex(uint32_t* d_keys, size_t n, dfr_stream_t stream, const dfr_config* cfg,
@@ -125,6 +140,8 @@ int dfr_sort_u32_ex(uint32_t* d_keys, size_t n, dfr_stream_t stream, const dfr_c
 int dfr_sort_u64_ex(uint64_t* d_keys, size_t n, dfr_stream_t stream, const dfr_config* cfg,
                     dfr_stats* stats);
 int dfr_sort_pairs_u32_ex(uint32_t* d_keys, uint32_t* d_vals, size_t n, dfr_stream_t stream,
+                          const dfr_config* cfg, dfr_stats* stats);
+int dfr_sort_pairs_u64_ex(uint64_t* d_keys, uint64_t* d_vals, size_t n, dfr_stream_t stream,
                           const dfr_config* cfg, dfr_stats* stats);
 
 /*

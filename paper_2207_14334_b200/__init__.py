@@ -14,7 +14,7 @@ import ctypes
 import os
 
 __all__ = [
-    "DfrError", "lib", "sort", "sort_u32", "sort_u64", "sort_pairs_u32", "histogram",
+    "DfrError", "lib", "sort", "sort_u32", "sort_u64", "sort_pairs_u32", "sort_pairs_u64", "histogram",
     "partition_pass", "top_passes", "workspace_bytes", "status_string", "EXPORTS", "overflow_mc",
 ]
 
@@ -23,8 +23,8 @@ LIB_PATH = os.environ.get("DFR_LIB") or os.path.join(_HERE, "libdfr.so")
 
 # every symbol include/dfr.h declares
 EXPORTS = (
-    "dfr_sort_u32", "dfr_sort_u64", "dfr_sort_pairs_u32",
-    "dfr_sort_u32_ex", "dfr_sort_u64_ex", "dfr_sort_pairs_u32_ex",
+    "dfr_sort_u32", "dfr_sort_u64", "dfr_sort_pairs_u32", "dfr_sort_pairs_u64",
+    "dfr_sort_u32_ex", "dfr_sort_u64_ex", "dfr_sort_pairs_u32_ex", "dfr_sort_pairs_u64_ex",
     "dfr_histogram_u32", "dfr_histogram_u64",
     "dfr_partition_pass_u64", "dfr_partition_pass_pairs_u32",
     "dfr_top_passes", "dfr_workspace_bytes", "dfr_launch_counter", "dfr_status_string",
@@ -43,7 +43,7 @@ class DfrError(RuntimeError):
 class Config(ctypes.Structure):
     _fields_ = [("n_d", ctypes.c_uint32), ("skip_trivial_passes", ctypes.c_uint32),
                 ("phase_events", ctypes.POINTER(ctypes.c_void_p)),
-                ("fused_last_pass", ctypes.c_uint32)]
+                ("fused_last_pass", ctypes.c_uint32), ("full_lsd", ctypes.c_uint32)]
 
 
 class Stats(ctypes.Structure):
@@ -73,6 +73,8 @@ def lib() -> ctypes.CDLL:
         "dfr_sort_u32": [p, sz, p],
         "dfr_sort_u64": [p, sz, p],
         "dfr_sort_pairs_u32": [p, p, sz, p],
+        "dfr_sort_pairs_u64": [p, p, sz, p],
+        "dfr_sort_pairs_u64_ex": [p, p, sz, p, cfgp, stp],
         "dfr_sort_u32_ex": [p, sz, p, cfgp, stp],
         "dfr_sort_u64_ex": [p, sz, p, cfgp, stp],
         "dfr_sort_pairs_u32_ex": [p, p, sz, p, cfgp, stp],
@@ -124,13 +126,13 @@ def _dev_tensor(t, widths):
     return t
 
 
-def _cfg(n_d, skip_trivial, events=None, fused=None):
+def _cfg(n_d, skip_trivial, events=None, fused=None, full_lsd=False):
     """events: None or a sequence of 2*len(PHASES) torch.cuda.Event(enable_timing=True)
     (None entries: that phase is not timed).
     fused: None (default: the fused last deal + diversion where eligible, dfr.h),
     True (same, explicit) or False (always the separate deal and diversion)."""
     mode = 0 if fused is None else (1 if fused else 2)
-    c = Config(int(n_d), 1 if skip_trivial else 0, None, mode)
+    c = Config(int(n_d), 1 if skip_trivial else 0, None, mode, 1 if full_lsd else 0)
     if events is not None:
         arr = (ctypes.c_void_p * len(events))(*[int(e.cuda_event) if e is not None else 0
                                                   for e in events])
@@ -144,13 +146,13 @@ def launch_counter() -> int:
 
 
 def sort_u32(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, events=None,
-             fused=None):
+             fused=None, full_lsd=False):
     """In-place ascending sort of a contiguous CUDA tensor of 32-bit keys (bit
     patterns read as uint32)."""
     _dev_tensor(keys, (4,))
     st = Stats() if stats else None
     rc = lib().dfr_sort_u32_ex(keys.data_ptr(), keys.numel(), _stream(stream),
-                               ctypes.byref(_cfg(n_d, skip_trivial, events, fused)),
+                               ctypes.byref(_cfg(n_d, skip_trivial, events, fused, full_lsd)),
                                ctypes.byref(st) if st is not None else None)
     _check(rc, "dfr_sort_u32")
     return st.as_dict() if st is not None else None
@@ -170,7 +172,7 @@ def sort_u64(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, event
 
 
 def sort_pairs_u32(keys, vals, *, n_d=64, skip_trivial=True, stream=None, stats=False,
-                   events=None, fused=None):
+                   events=None, fused=None, full_lsd=False):
     """Stable in-place sort of (uint32 key, uint32 value) pairs held in two
     contiguous CUDA tensors of equal length."""
     _dev_tensor(keys, (4,))
@@ -179,15 +181,35 @@ def sort_pairs_u32(keys, vals, *, n_d=64, skip_trivial=True, stream=None, stats=
         raise DfrError("keys and vals differ in length")
     st = Stats() if stats else None
     rc = lib().dfr_sort_pairs_u32_ex(keys.data_ptr(), vals.data_ptr(), keys.numel(),
-                                     _stream(stream), ctypes.byref(_cfg(n_d, skip_trivial, events, fused)),
+                                     _stream(stream),
+                                     ctypes.byref(_cfg(n_d, skip_trivial, events, fused, full_lsd)),
                                      ctypes.byref(st) if st is not None else None)
     _check(rc, "dfr_sort_pairs_u32")
     return st.as_dict() if st is not None else None
 
 
+def sort_pairs_u64(keys, vals, *, n_d=64, skip_trivial=True, stream=None, stats=False,
+                   events=None, fused=None):
+    """Stable in-place sort of (uint64 key, uint64 value) records held in two
+    contiguous CUDA tensors of 8-byte elements and equal length."""
+    _dev_tensor(keys, (8,))
+    _dev_tensor(vals, (8,))
+    if keys.numel() != vals.numel():
+        raise DfrError("keys and vals differ in length")
+    st = Stats() if stats else None
+    rc = lib().dfr_sort_pairs_u64_ex(keys.data_ptr(), vals.data_ptr(), keys.numel(),
+                                     _stream(stream), ctypes.byref(_cfg(n_d, skip_trivial, events, fused)),
+                                     ctypes.byref(st) if st is not None else None)
+    _check(rc, "dfr_sort_pairs_u64")
+    return st.as_dict() if st is not None else None
+
+
 def sort(keys, vals=None, **kw):
-    """Dispatch on key width: 4-byte keys -> u32 (pairs if ``vals``), 8-byte -> u64."""
+    """Dispatch on widths: 4-byte keys -> u32 (pairs if ``vals``), 8-byte keys
+    -> u64 (pairs with 8-byte ``vals``)."""
     if vals is not None:
+        if keys.element_size() == 8:
+            return sort_pairs_u64(keys, vals, **kw)
         return sort_pairs_u32(keys, vals, **kw)
     if keys.element_size() == 8:
         return sort_u64(keys, **kw)

@@ -393,11 +393,15 @@ static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals,
   return P;
 }
 
-static int cfg_nd(const dfr_config* cfg, uint32_t* n_d, uint32_t* skip, uint32_t* nofuse) {
+static int cfg_nd(const dfr_config* cfg, uint32_t* n_d, uint32_t* skip, uint32_t* nofuse,
+                  uint32_t* full_lsd) {
   *n_d = DFR_DEFAULT_ND;
   *skip = 1;
   *nofuse = 0;
+  *full_lsd = 0;
   if (cfg) {
+    if (cfg->full_lsd > 1) return DFR_ERR_INVALID;
+    *full_lsd = cfg->full_lsd;
     *n_d = cfg->n_d ? cfg->n_d : DFR_DEFAULT_ND;
     *skip = cfg->skip_trivial_passes ? 1 : 0;
     if (cfg->fused_last_pass > 2) return DFR_ERR_INVALID;
@@ -411,8 +415,9 @@ template <class K, bool PAIRS>
 static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const dfr_config* cfg,
                      dfr_stats* stats) {
   using Ph = Phases<K, PAIRS>;
-  uint32_t n_d, skip, nofuse;
-  if (cfg_nd(cfg, &n_d, &skip, &nofuse) != DFR_OK) return DFR_ERR_INVALID;
+  uint32_t n_d, skip, nofuse, full_lsd;
+  if (cfg_nd(cfg, &n_d, &skip, &nofuse, &full_lsd) != DFR_OK) return DFR_ERR_INVALID;
+  if (full_lsd && sizeof(K) > (size_t)MAX_PASSES) return DFR_ERR_INVALID;  // D = 8 > passes a group holds
   if (stats) memset(stats, 0, sizeof(*stats));
   if (n <= 1) return DFR_OK;
   if (!keys || (PAIRS && !vals)) return DFR_ERR_INVALID;
@@ -429,11 +434,11 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
   cudaGetLastError();
 
   int p0 = est_top_passes(n, n_d);
-  if (p0 > (int)sizeof(K)) p0 = (int)sizeof(K);
+  if (p0 > (int)sizeof(K) || full_lsd) p0 = (int)sizeof(K);
   // fused last pass (Phases::fused): large keys-only top calls with 3 group
   // digits (s-runs of about n / 2^16 >= 2048 keys fill a tile)
   const bool fuse = !PAIRS && !nofuse && p0 == 3 && n >= ((size_t)1 << 27);
-  const Layout L = make_layout(n, sizeof(K), PAIRS ? 4 : 0, n_d, 1, fuse);
+  const Layout L = make_layout(n, sizeof(K), PAIRS ? 4 : 0, n_d, full_lsd ? (int)sizeof(K) : 1, fuse);
   char* ws = nullptr;
   if (cudaMallocAsync(reinterpret_cast<void**>(&ws), L.total, st) != cudaSuccess) {
     cudaGetLastError();
@@ -441,6 +446,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
   }
   Params<K> P = make_params<K>(ws, L, keys, vals, PAIRS, n_d, skip, n);
   P.fuse = fuse ? 1u : 0u;
+  P.full_lsd = full_lsd;
   const uint32_t nn = (uint32_t)n;
   const int sms = dv.sms;
   const PhaseEv pe{cfg ? cfg->phase_events : nullptr, st};
@@ -601,6 +607,53 @@ static int stage_impl(const K* in, const uint32_t* vin, K* out, uint32_t* vout, 
   return e == cudaSuccess ? DFR_OK : DFR_ERR_CUDA;
 }
 
+// (u64 key, u64 value) records (SPEC's 16-byte Record): the keys are
+// sorted stably with their u32 input positions as the payload (the pairs
+// path), then the values follow through that permutation.
+__global__ void k_iota(uint32_t* v, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
+}
+__global__ void k_gather_u64(const unsigned long long* src, const uint32_t* idx, unsigned long long* dst,
+                             uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+static int sort_pairs_u64(unsigned long long* keys, unsigned long long* vals, size_t n, cudaStream_t st,
+                          const dfr_config* cfg, dfr_stats* stats) {
+  if (stats) memset(stats, 0, sizeof(*stats));
+  if (n <= 1) return DFR_OK;
+  if (!keys || !vals) return DFR_ERR_INVALID;
+  if ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(vals)) % 8) return DFR_ERR_INVALID;
+  {
+    const char* ka = reinterpret_cast<const char*>(keys);
+    const char* va = reinterpret_cast<const char*>(vals);
+    if (ka < va + n * 8 && va < ka + n * 8) return DFR_ERR_INVALID;
+  }
+  if (n >= DFR_MAX_N) return DFR_ERR_TOO_LARGE;
+  Dev dv;
+  if (get_dev<unsigned long long, true>(dv) != cudaSuccess) return DFR_ERR_CUDA;
+  char* ws = nullptr;
+  const size_t idx_bytes = align_up(n * 4);
+  if (cudaMallocAsync(reinterpret_cast<void**>(&ws), idx_bytes + n * 8, st) != cudaSuccess) {
+    cudaGetLastError();
+    return DFR_ERR_ALLOC;
+  }
+  uint32_t* idx = reinterpret_cast<uint32_t*>(ws);
+  unsigned long long* tmp = reinterpret_cast<unsigned long long*>(ws + idx_bytes);
+  const int grid = 4 * dv.sms;
+  k_iota<<<grid, 256, 0, st>>>(idx, (uint32_t)n);
+  int rc = sort_impl<unsigned long long, true>(keys, idx, n, st, cfg, stats);
+  if (rc == DFR_OK) {
+    k_gather_u64<<<grid, 256, 0, st>>>(vals, idx, tmp, (uint32_t)n);
+    if (cudaMemcpyAsync(vals, tmp, n * 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess) rc = DFR_ERR_CUDA;
+    g_launches += 2;
+    if (rc == DFR_OK && cudaGetLastError() != cudaSuccess) rc = DFR_ERR_CUDA;
+  }
+  if (cudaFreeAsync(ws, st) != cudaSuccess && rc == DFR_OK) rc = DFR_ERR_CUDA;
+  return rc;
+}
+
 }  // namespace dfr
 
 // -------------------------------------------------------------------- C ABI
@@ -627,6 +680,15 @@ int dfr_sort_u64(uint64_t* d_keys, size_t n, dfr_stream_t stream) {
 }
 int dfr_sort_pairs_u32(uint32_t* d_keys, uint32_t* d_vals, size_t n, dfr_stream_t stream) {
   return dfr_sort_pairs_u32_ex(d_keys, d_vals, n, stream, nullptr, nullptr);
+}
+int dfr_sort_pairs_u64_ex(uint64_t* d_keys, uint64_t* d_vals, size_t n, dfr_stream_t stream,
+                          const dfr_config* cfg, dfr_stats* stats) {
+  return dfr::sort_pairs_u64(reinterpret_cast<unsigned long long*>(d_keys),
+                             reinterpret_cast<unsigned long long*>(d_vals), n, (cudaStream_t)stream, cfg,
+                             stats);
+}
+int dfr_sort_pairs_u64(uint64_t* d_keys, uint64_t* d_vals, size_t n, dfr_stream_t stream) {
+  return dfr_sort_pairs_u64_ex(d_keys, d_vals, n, stream, nullptr, nullptr);
 }
 
 int dfr_histogram_u32(const uint32_t* d_keys, size_t n, int digit_lo, int p, uint32_t* d_counts,

@@ -165,6 +165,7 @@ struct Params {
   uint32_t* J;          // fused level 0: [256][16] counts of (top digit, top 4 bits of the
                         // middle digit), then [16][256] chain bases (exclusive over chains)
   uint32_t skip_trivial;
+  uint32_t full_lsd;    // ablation: the top call sorts all D digits LSD (dfr_config.full_lsd)
   int D;                // digits per key
   __device__ __forceinline__ K* kbuf(uint32_t id) const { return id == 0 ? A : (id == 1 ? B : C); }
   __device__ __forceinline__ uint32_t* vbuf(uint32_t id) const {

@@ -127,7 +127,7 @@ struct Phases {
           if (!s.buf) chunks = 0;
         } else {
           int pp = est_top_passes(s.len, P.n_d);
-          if (pp > s.hi + 1) pp = s.hi + 1;
+          if (pp > s.hi + 1 || (P.full_lsd && c->level + 1u == 0u)) pp = s.hi + 1;  // (ablation: all digits)
           p = (uint32_t)pp;
           s.p = p;
           s.low = s.hi - pp + 1;
@@ -447,7 +447,7 @@ struct Phases {
       // recursion levels: when the passes end on digit 0 every bucket of the
       // scan (Alg. 4 l.8) is a constant key -- insertion sort and recursion
       // leave it as it is -- so the diversion only moves the segment to A
-      if (executed > 0 && s.low == 0 && c->level > 0) flags |= SEG_SORTED;
+      if (executed > 0 && s.low == 0 && (c->level > 0 || P.full_lsd)) flags |= SEG_SORTED;
       // buffer route of the executed passes: ping-pong between the data's
       // buffer and another one; a level 0 with the second scratch buffer runs
       // A -> C -> B -> C, so that its third pass (the fused pass, B -> A)

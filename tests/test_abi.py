@@ -20,7 +20,7 @@ def _declared():
 def test_library_exports_every_declared_symbol():
     L = dfr.lib()
     decl = _declared()
-    assert len(decl) == 15
+    assert len(decl) == 17
     assert sorted(dfr.EXPORTS) == decl
     for name in decl:
         assert hasattr(L, name), name
@@ -46,9 +46,15 @@ def test_trivial_calls_need_no_device():
     assert L.dfr_sort_u64(None, 0, None) == 0
     assert L.dfr_sort_u32(None, 1, None) == 0
     assert L.dfr_sort_pairs_u32(None, None, 0, None) == 0
+    assert L.dfr_sort_pairs_u64(None, None, 1, None) == 0
+    assert L.dfr_sort_pairs_u64(None, None, 10, None) == dfr.DFR_ERR_INVALID
     # bad configuration is rejected up front
     bad = dfr.Config(3, 1)
     assert L.dfr_sort_u64_ex(None, 10, None, ctypes.byref(bad), None) == dfr.DFR_ERR_INVALID
+    bad = dfr.Config(64, 1, None, 3)  # fused_last_pass out of range
+    assert L.dfr_sort_u64_ex(None, 10, None, ctypes.byref(bad), None) == dfr.DFR_ERR_INVALID
+    lsd = dfr.Config(64, 1, None, 0, 1)  # the full-LSD ablation holds 4 digits: not u64
+    assert L.dfr_sort_u64_ex(ctypes.c_void_p(0x1000), 10, None, ctypes.byref(lsd), None) == dfr.DFR_ERR_INVALID
     # null pointer with n > 1
     assert L.dfr_sort_u64(None, 10, None) == dfr.DFR_ERR_INVALID
     # misaligned element pointer

@@ -119,3 +119,41 @@ def test_concurrent_streams():
         rk, rv, _ = oracle.dfr_sort(kb, vb)
         _same(to_host(b, np.uint32), rk, "stream 2 keys")
         _same(to_host(bv, np.uint32), rv, "stream 2 values")
+
+
+@pytest.mark.parametrize("case,n", [("uniform", 1000), ("uniform", 300007), ("uniform", (1 << 21) + 3),
+                                    ("uniform", (1 << 22) + 5), ("uniform", 1 << 24),
+                                    ("few", (1 << 22) + 1), ("zipf", 1 << 22), ("equal", 100003)])
+def test_u64_pairs(case, n):
+    """dfr_sort_pairs_u64: (u64 key, u64 tag) records (SPEC's Record),
+    stable: equal keys keep input order; keys and tags bit-exact vs the
+    oracle's pairs sort."""
+    if case == "uniform":
+        k = datagen.uniform_u64(n, 211)
+    elif case == "few":
+        k = datagen.uniform_u64(256, 212)[datagen.uniform_u64(n, 213) >> np.uint64(56)]
+    elif case == "zipf":
+        k = datagen.zipf_u64(n, 214)
+    else:
+        k = np.full(n, 0x0123456789ABCDEF, np.uint64)
+    v = datagen.uniform_u64(n, 215, "tags")
+    gk, gv, st = gpu_sort(k, v, stats=True)
+    rk, rv, _ = oracle.dfr_sort(k, v)
+    assert st["overflow"] == 0
+    _same(gk, rk, "keys")
+    _same(gv, rv, "values (stability)")
+
+
+@pytest.mark.parametrize("n", [(1 << 20) + 7, (1 << 23) + 3])
+def test_full_lsd_ablation_u32(n):
+    """dfr_config.full_lsd (SPEC AC7): the top call is a plain LSD sort
+    over all four digits -- the same output as DFR (keys and stable pairs)."""
+    k = datagen.uniform_u32(n, 221)
+    gk, _, st = gpu_sort(k, stats=True, full_lsd=True)
+    assert st["level0_p"] == 4
+    _same(gk, oracle.dfr_sort(k)[0], "keys")
+    kp, vp = datagen.make_case("c4-few", n)
+    gk, gv, st = gpu_sort(kp, vp, stats=True, full_lsd=True)
+    rk, rv, _ = oracle.dfr_sort(kp, vp)
+    _same(gk, rk, "pair keys")
+    _same(gv, rv, "pair values")
