@@ -61,6 +61,8 @@ def parse():
                          "between kernels stop programmatic dependent launch from overlapping "
                          "them); the per-phase times always come from a separate run of K steps")
     ap.add_argument("--no-cold", action="store_true", help="skip the cold-pool trial")
+    ap.add_argument("--fast-radix", action="store_true",
+                    help="dfr_config.fast_radix = 1 (Fast Radix estimation of the first group pass)")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     return ap.parse_args()
 
@@ -248,7 +250,8 @@ def run_dfr(args, rank, world, local_rank):
     def sort_step(i, ev=None):
         b = bufs[i % nbuf]
         vbuf = vbufs[i % nbuf]
-        dfr.sort(b, vbuf, events=ev, fused=None if args.fused == "auto" else False)
+        kw = {"fast_radix": True} if args.fast_radix else {}
+        dfr.sort(b, vbuf, events=ev, fused=None if args.fused == "auto" else False, **kw)
 
     def restore_buf(i):
         bufs[i % nbuf].copy_(pristine)

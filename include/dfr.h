@@ -82,6 +82,15 @@ typedef struct dfr_config {
                                diversion, no recursion).  u32 keys and u32 pairs only
                                (D = 4); DFR_ERR_INVALID for u64 keys.  Inputs of at most
                                4096 keys still run the on-chip DFR. */
+  uint32_t fast_radix;      /* 0 (default).  1: Fast Radix estimation (§3, Alg. 3,
+                               P:211-246) on the fused level-0 path (keys only, p = 3,
+                               n >= 2^27; ignored elsewhere): the pass on the lowest group
+                               digit deals into estimated buckets of ceil(n/256) keys
+                               with overflow chunks instead of reading a histogram first,
+                               counting the middle digit; the middle pass reads bucket by
+                               bucket and counts the top digit (the top digit counted in the
+                               penultimate pass, Alg. 3 l.5-6).  No pass is skipped.
+                               Same output. */
 } dfr_config;
 
 /* Phases timed through dfr_config.phase_events. */
@@ -105,6 +114,8 @@ typedef struct dfr_stats {
   uint32_t levels;            /* recursion levels executed after level 0 */
   uint32_t overflow;          /* device queue overflow flags (0 = none; non-zero = bug) */
   uint32_t fused;             /* 1: the top call ran the fused last deal + diversion */
+  uint32_t fr_overflow;       /* Fast Radix: records the estimated pass dealt to overflow
+                                 space (beyond their bucket's estimated capacity) */
 } dfr_stats;
 
 /*

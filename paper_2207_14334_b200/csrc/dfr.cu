@@ -125,6 +125,31 @@ __global__ void __launch_bounds__(Phases<K, false>::SC_NT, 4) k_scatter_fh(const
   Phases<K, false>::template scatter<Phases<K, false>::SC_NT, true, true>(P, j, sm);
 }
 
+// Fast Radix (dfr_config.fast_radix, keys only): the estimated pass on the
+// lowest group digit, its plan, and the middle pass reading the estimated layout
+template <class K>
+__global__ void __launch_bounds__(THREADS) k_fr_prep(const __grid_constant__ Params<K> P) {
+  pdl_enter();
+  Phases<K, false>::fr_prep(P);
+}
+template <class K>
+__global__ void __launch_bounds__(Phases<K, false>::SC_NT, 4) k_scatter_fr(const __grid_constant__ Params<K> P, int j) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  pdl_enter();
+  Phases<K, false>::template scatter<Phases<K, false>::SC_NT, false, true, 1>(P, j, sm);
+}
+template <class K>
+__global__ void __launch_bounds__(THREADS) k_fr_plan(const __grid_constant__ Params<K> P) {
+  pdl_enter();
+  Phases<K, false>::fr_plan(P);
+}
+template <class K>
+__global__ void __launch_bounds__(Phases<K, false>::SC_NT, 4) k_scatter_frfh(const __grid_constant__ Params<K> P, int j) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  pdl_enter();
+  Phases<K, false>::template scatter<Phases<K, false>::SC_NT, true, true, 2>(P, j, sm);
+}
+
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(Phases<K, PAIRS>::DV_NT, DFR_DV_MINB) k_divert(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
@@ -289,6 +314,12 @@ static cudaError_t get_dev(Dev& out) {
     if (err == cudaSuccess && !PAIRS)
       err = cudaFuncSetAttribute((const void*)k_scatter_fh<K>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_SCATTER_P);
+    if (err == cudaSuccess && !PAIRS)
+      err = cudaFuncSetAttribute((const void*)k_scatter_fr<K>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_SCATTER_P);
+    if (err == cudaSuccess && !PAIRS)
+      err = cudaFuncSetAttribute((const void*)k_scatter_frfh<K>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_SCATTER_P);
     if (err == cudaSuccess) {  // the deal (one tile buffer + permutation)
       err = cudaFuncSetAttribute((const void*)k_scatter<K, PAIRS>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_SCATTER_P);
@@ -324,11 +355,12 @@ static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a
 
 struct Layout {
   size_t b_keys, b_vals, c_keys, ctl, segq0, segq1, midq, hist, status, fh, ftiles, fj, total;
+  size_t fr_ct, fr_tab, fr_cnt, fr_cap, fr_kmax;
   size_t max_segs, mid_cap, hist_rows, tiles_max;
 };
 
 static Layout make_layout(size_t n, int kb, int vb, uint32_t n_d, int min_passes = 1,
-                          bool fuse = false) {
+                          bool fuse = false, bool fr = false) {
   Layout L{};
   L.max_segs = n / (MID_CAP + 1) + 2;
   L.mid_cap = n / (n_d + 1) + 2;
@@ -345,7 +377,14 @@ static Layout make_layout(size_t n, int kb, int vb, uint32_t n_d, int min_passes
   };
   L.b_keys = take(n * kb);
   L.b_vals = vb ? take(n * vb) : 0;
-  L.c_keys = fuse ? take(n * kb) : 0;  // fused level 0: A -> C -> B, fused pass B -> A
+  // fused level 0: A -> C -> B, fused pass B -> A.  Fast Radix: C holds the
+  // 256 estimated buckets of ceil(n/256) keys, then overflow chunks (at most
+  // n keys in all, plus one partly used chunk per bucket)
+  using PhK = Phases<unsigned long long, false>;
+  L.fr_cap = (n + 255) / 256;
+  L.fr_kmax = n / PhK::FR_CHUNK + 2;
+  const size_t c_elems = fr ? 256 * L.fr_cap + n + 256 * (size_t)PhK::FR_CHUNK : n;
+  L.c_keys = fuse ? take(c_elems * kb) : 0;
   L.ctl = take(sizeof(Ctl));
   L.segq0 = take(L.max_segs * sizeof(Seg));
   L.segq1 = take(L.max_segs * sizeof(Seg));
@@ -358,6 +397,9 @@ static Layout make_layout(size_t n, int kb, int vb, uint32_t n_d, int min_passes
   L.fh = fuse ? take(65536 * 4) : 0;      // joint histogram of the two low group digits
   L.ftiles = fuse ? take(65536 * 16) : 0;  // run-aligned tiles of the fused pass
   L.fj = fuse ? take(2 * 4096 * 4) : 0;     // chain histogram and bases of the fused pass
+  L.fr_ct = fr ? take(256 * L.fr_kmax * 4) : 0;                 // Fast Radix chunk table
+  L.fr_tab = fr ? take((2 * (n / TILE) + 2 * 256 + 8) * 8) : 0;  // tiles of the middle pass
+  L.fr_cnt = fr ? take(512 * 4) : 0;
   L.total = off;
   return L;
 }
@@ -383,6 +425,12 @@ static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals,
   P.H = L.fh ? reinterpret_cast<uint32_t*>(ws + L.fh) : nullptr;
   P.ftiles = L.ftiles ? reinterpret_cast<uint4*>(ws + L.ftiles) : nullptr;
   P.J = L.fj ? reinterpret_cast<uint32_t*>(ws + L.fj) : nullptr;
+  P.fr = L.fr_ct ? 1u : 0u;
+  P.fr_cap = (uint32_t)L.fr_cap;
+  P.fr_kmax = (uint32_t)L.fr_kmax;
+  P.fr_ct = L.fr_ct ? reinterpret_cast<uint32_t*>(ws + L.fr_ct) : nullptr;
+  P.fr_tab = L.fr_tab ? reinterpret_cast<uint2*>(ws + L.fr_tab) : nullptr;
+  P.fr_cnt = L.fr_cnt ? reinterpret_cast<uint32_t*>(ws + L.fr_cnt) : nullptr;
   P.max_segs = (uint32_t)L.max_segs;
   P.mid_cap = (uint32_t)L.mid_cap;
   P.hist_rows = (uint32_t)L.hist_rows;
@@ -394,12 +442,15 @@ static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals,
 }
 
 static int cfg_nd(const dfr_config* cfg, uint32_t* n_d, uint32_t* skip, uint32_t* nofuse,
-                  uint32_t* full_lsd) {
+                  uint32_t* full_lsd, uint32_t* fast_radix) {
   *n_d = DFR_DEFAULT_ND;
   *skip = 1;
   *nofuse = 0;
   *full_lsd = 0;
+  *fast_radix = 0;
   if (cfg) {
+    if (cfg->fast_radix > 1) return DFR_ERR_INVALID;
+    *fast_radix = cfg->fast_radix;
     if (cfg->full_lsd > 1) return DFR_ERR_INVALID;
     *full_lsd = cfg->full_lsd;
     *n_d = cfg->n_d ? cfg->n_d : DFR_DEFAULT_ND;
@@ -415,8 +466,8 @@ template <class K, bool PAIRS>
 static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const dfr_config* cfg,
                      dfr_stats* stats) {
   using Ph = Phases<K, PAIRS>;
-  uint32_t n_d, skip, nofuse, full_lsd;
-  if (cfg_nd(cfg, &n_d, &skip, &nofuse, &full_lsd) != DFR_OK) return DFR_ERR_INVALID;
+  uint32_t n_d, skip, nofuse, full_lsd, fast_radix;
+  if (cfg_nd(cfg, &n_d, &skip, &nofuse, &full_lsd, &fast_radix) != DFR_OK) return DFR_ERR_INVALID;
   if (full_lsd && sizeof(K) > (size_t)MAX_PASSES) return DFR_ERR_INVALID;  // D = 8 > passes a group holds
   if (stats) memset(stats, 0, sizeof(*stats));
   if (n <= 1) return DFR_OK;
@@ -438,7 +489,9 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
   // fused last pass (Phases::fused): large keys-only top calls with 3 group
   // digits (s-runs of about n / 2^16 >= 2048 keys fill a tile)
   const bool fuse = !PAIRS && !nofuse && p0 == 3 && n >= ((size_t)1 << 27);
-  const Layout L = make_layout(n, sizeof(K), PAIRS ? 4 : 0, n_d, full_lsd ? (int)sizeof(K) : 1, fuse);
+  // Fast Radix estimation (Alg. 3): on the fused level-0 path
+  const bool fr = fuse && fast_radix && !full_lsd;
+  const Layout L = make_layout(n, sizeof(K), PAIRS ? 4 : 0, n_d, full_lsd ? (int)sizeof(K) : 1, fuse, fr);
   char* ws = nullptr;
   if (cudaMallocAsync(reinterpret_cast<void**>(&ws), L.total, st) != cudaSuccess) {
     cudaGetLastError();
@@ -482,21 +535,37 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
     g_launches += 2;
   } else {
     const uint32_t tiles = (nn + TILE - 1) / TILE;
+    const int g_hist = (int)std::min<uint32_t>(tiles, (uint32_t)(sms * std::max(1, dv.occ_hist)));
+    const int g_sc = (int)std::min<uint32_t>(tiles, (uint32_t)(sms * std::max(1, dv.occ_scatter)));
     pe.begin(DFR_PHASE_HIST);
     k_init<K, PAIRS><<<1, THREADS, 64, st>>>(P, nn);
-    const int g_hist = (int)std::min<uint32_t>(tiles, (uint32_t)(sms * std::max(1, dv.occ_hist)));
-    launch_pdl(k_hist<K, PAIRS>, g_hist, THREADS, Ph::SMEM_HIST, st, P);
+    if (fr) {  // Fast Radix: no histogram read of the input
+      launch_pdl(k_fr_prep<K>, 4 * sms, THREADS, 0, st, P);
+    } else {
+      launch_pdl(k_hist<K, PAIRS>, g_hist, THREADS, Ph::SMEM_HIST, st, P);
+    }
     pe.end(DFR_PHASE_HIST);
     pe.begin(DFR_PHASE_PLAN);
-    launch_pdl(k_plan2<K, PAIRS>, 1, THREADS, 64, st, P);
+    if (!fr) launch_pdl(k_plan2<K, PAIRS>, 1, THREADS, 64, st, P);
     pe.end(DFR_PHASE_PLAN);
-    const int g_sc = (int)std::min<uint32_t>(tiles, (uint32_t)(sms * std::max(1, dv.occ_scatter)));
     for (int j = 0; j < MAX_PASSES; ++j) {
       if (j >= p0) {
         pe.skip(DFR_PHASE_SCATTER0 + j);
         continue;
       }
       pe.begin(DFR_PHASE_SCATTER0 + j);
+      if (fr && j < 2) {  // the estimated pass, its plan, the pass reading the estimated layout
+        if (j == 0) {
+          launch_pdl(k_scatter_fr<K>, g_sc, Ph::SC_NT, Ph::SMEM_SCATTER_P, st, P, 0);
+          launch_pdl(k_fr_plan<K>, 1, THREADS, 0, st, P);
+        } else {
+          const int g_fr = sms * std::max(1, dv.occ_scatter);
+          launch_pdl(k_scatter_frfh<K>, g_fr, Ph::SC_NT, Ph::SMEM_SCATTER_P, st, P, 1);
+        }
+        g_launches += j == 0 ? 2 : 1;
+        pe.end(DFR_PHASE_SCATTER0 + j);
+        continue;
+      }
       if (fuse && j == 2) {  // run-aligned tiles, then the fused last deal + diversion
         launch_pdl(k_fplan<K, PAIRS>, 1, 1024, 0, st, P);
         const int g_f = sms * std::max(1, dv.occ_fused);
@@ -558,6 +627,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
       stats->levels = h.levels_run;
       stats->overflow = h.overflow;
       stats->fused = h.fused_ok;
+      stats->fr_overflow = h.fr_overflow;
     }
   }
   if (cudaFreeAsync(ws, st) != cudaSuccess && rc == DFR_OK) rc = DFR_ERR_CUDA;

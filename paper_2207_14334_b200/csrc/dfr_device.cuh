@@ -134,7 +134,11 @@ struct Ctl {
   uint32_t fused_ok;            // level 0 ran the fused last pass (plan kernel's verdict)
   uint32_t fused_tiles;         // run-aligned tiles of the fused pass
   uint32_t fticket;             // dynamic tile ticket of the fused pass
-  uint32_t fused_pad;
+  uint32_t fused_regular;       // fused pass: tickets below this have chain predecessor ticket - chains
+  uint32_t fused_chains;        // fused pass: look-back chains (16, or 1 without the chain histogram)
+  uint32_t fr_next_chunk;       // Fast Radix: overflow chunks handed out so far
+  uint32_t fr_tiles;            // Fast Radix: tiles of the pass that reads the estimated layout
+  uint32_t fr_overflow;         // Fast Radix: records the estimated pass dealt to overflow
 };
 
 template <class K>
@@ -166,6 +170,19 @@ struct Params {
                         // middle digit), then [16][256] chain bases (exclusive over chains)
   uint32_t skip_trivial;
   uint32_t full_lsd;    // ablation: the top call sorts all D digits LSD (dfr_config.full_lsd)
+  // Fast Radix estimation (dfr_config.fast_radix; Alg. 3): the
+  // level-0 pass on the lowest group digit deals into ESTIMATED buckets of
+  // fr_cap = ceil(n/256) keys at d * fr_cap of its destination buffer; a key
+  // ranked past its bucket's capacity goes to the overflow chunk of
+  // FR_CHUNK keys its bucket's rank falls in (chunks handed out on first
+  // touch, after the 256 main regions: "virtually extending overflown
+  // buckets"); the next pass reads bucket by bucket, main region then chunks.
+  uint32_t fr;          // 1: level 0 runs Fast Radix estimation
+  uint32_t fr_cap;
+  uint32_t fr_kmax;     // chunk-table columns per bucket
+  uint32_t* fr_ct;      // [256][fr_kmax] chunk id + 1 (0: not handed out; ~0u: being handed out)
+  uint2* fr_tab;        // tiles of the pass that reads the estimated layout: (offset, length)
+  uint32_t* fr_cnt;     // [2][256]: next-digit counts (exact offsets of the next pass), top-digit counts
   int D;                // digits per key
   __device__ __forceinline__ K* kbuf(uint32_t id) const { return id == 0 ? A : (id == 1 ? B : C); }
   __device__ __forceinline__ uint32_t* vbuf(uint32_t id) const {

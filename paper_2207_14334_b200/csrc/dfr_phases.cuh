@@ -72,7 +72,7 @@ struct Phases {
   // The deal kernel runs SC_NT threads per CTA over tiles of TILE keys
   // (4 CTAs/SM with the permutation deal: 32 warps hide the look-back and load latencies)
   static constexpr int SC_NT = 256;
-  static constexpr int SCATTER_HDR_WORDS = (SC_NT / 32 + 1) * 256 + 256 + 32;
+  static constexpr int SCATTER_HDR_WORDS = (SC_NT / 32 + 1) * 256 + 256 + 32 + 256;
   static constexpr size_t SMEM_SCATTER =
       SCATTER_HDR_WORDS * 4 + 2 * TILE * sizeof(K) + (PAIRS ? 2 * TILE * 4 : 0);
   // PERM deal: header | permutation | one tile
@@ -498,13 +498,36 @@ struct Phases {
   // reordered as a permutation of positions (u16, `perm`) and the write-out
   // gathers keys through it — 32 fewer registers per thread (u64), which lets
   // 4 CTAs share an SM.
-  template <int SC_NT, bool FULL, bool FUSEH, bool PERM, class Hook>
+  // Fast Radix: the overflow chunk of bucket d holding its overflow ranks
+  // [k * FR_CHUNK, (k+1) * FR_CHUNK): handed out on first touch (a lock word
+  // while the id is drawn)
+  static constexpr uint32_t FR_CHUNK = 4096, FR_LOCK = ~0u;
+  static __device__ __forceinline__ uint32_t fr_chunk(const Params<K>& P, uint32_t d, uint32_t k) {
+    uint32_t* e = P.fr_ct + (size_t)d * P.fr_kmax + k;
+    uint32_t v = *(volatile uint32_t*)e;
+    if (v == 0u) {
+      v = atomicCAS(e, 0u, FR_LOCK);
+      if (v == 0u) {
+        v = atomicAdd(&P.ctl->fr_next_chunk, 1u) + 1u;
+        atomicExch(e, v);
+        return v - 1u;
+      }
+    }
+    while (v == FR_LOCK) v = *(volatile uint32_t*)e;
+    return v - 1u;
+  }
+
+  // FRM (Fast Radix mode): 0 counted deal; 1 deal into estimated buckets (with
+  // overflow chunks), counting the next digit; 2 deal reading the estimated
+  // layout through the tile table, counting the next (top) digit
+  template <int SC_NT, bool FULL, bool FUSEH, bool PERM, int FRM = 0, class Hook>
   static __device__ __forceinline__ void deal_tile(const Hook& after_lookback, const Params<K>& P,
                                                    const Seg& s, int j,
                                                    uint32_t t, uint32_t lt, uint32_t cnt, int dg,
                                                    uint32_t* status, K* sk, V* sv, uint32_t* whist,
                                                    int* s_dst, uint32_t* s_warp, K* dst, V* dstv,
-                                                   uint32_t bstart, uint16_t* perm, uint32_t sup) {
+                                                   uint32_t bstart, uint16_t* perm, uint32_t sup,
+                                                   uint32_t nh_s = 0) {
     constexpr int SC_W = SC_NT / 32;
     constexpr int SC_KPT = TILE / SC_NT;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -521,7 +544,10 @@ struct Phases {
       key[jj] = sk[(PERM ? (sup & 0xffu) : 0u) + idx];  // PERM: the tile starts koff into sk
       if (PAIRS && !PERM) val[jj] = sv[idx];
       dr[jj] = (FULL || idx < cnt) ? digit_of(key[jj], dg) : 256u;
-      if (FULL || idx < cnt) red_add_shared(tc_s + 4 * dr[jj], 1u);  // tile histogram
+      if (FULL || idx < cnt) {
+        red_add_shared(tc_s + 4 * dr[jj], 1u);  // tile histogram
+        if (FRM) red_add_shared(nh_s + 4 * digit_of(key[jj], dg + 1), 1u);  // the next digit (Alg. 3 l.5-6)
+      }
     }
     __syncthreads();
     if (FUSEH) {  // joint histogram [this digit][digit below] for the fused last pass
@@ -633,7 +659,8 @@ struct Phases {
         st_relaxed(status + (size_t)t * 256 + dd, FLAG_INC | (excl + run));
       }
       // run offset of the digit relative to the tile's local offsets, mod 2^32
-      s_dst[dd] = (int)(s.start + bstart + excl - lstart);
+      // (Fast Radix estimated pass: the rank inside the digit's bucket)
+      s_dst[dd] = FRM == 1 ? (int)(excl - lstart) : (int)(s.start + bstart + excl - lstart);
     }
 #if DFR_CLAIM_AFTER_BARRIER
     __syncthreads();
@@ -647,9 +674,18 @@ struct Phases {
     for (uint32_t i = threadIdx.x; i < (FULL ? (uint32_t)TILE : cnt); i += SC_NT) {
       const uint32_t src = PERM ? (uint32_t)perm[i] : i;
       const K k = sk[src];
-      const uint32_t o = (uint32_t)s_dst[digit_of(k, dg)] + i;  // < 2^30: unsigned math
+      const uint32_t dk = digit_of(k, dg);
+      uint32_t o = (uint32_t)s_dst[dk] + i;  // < 2^30: unsigned math
+      if (FRM == 1) {  // estimated bucket dk: main region, or the overflow chunk of rank o
+        if (o < P.fr_cap) {
+          o += dk * P.fr_cap;
+        } else {
+          const uint32_t ov = o - P.fr_cap;
+          o = 256u * P.fr_cap + fr_chunk(P, dk, ov / FR_CHUNK) * FR_CHUNK + ov % FR_CHUNK;
+        }
+      }
 #ifdef DFR_DEBUG
-      if (o < s.start || o >= s.start + s.len) {
+      if (FRM != 1 && (o < s.start || o >= s.start + s.len)) {
         printf("scatter OOB: t=%u i=%u o=%u seg=[%u,%u)\n", t, i, o, s.start, s.start + s.len);
         __trap();
       }
@@ -673,7 +709,23 @@ struct Phases {
   // SUP: the copy covers the 16-byte aligned superset of the tile (the tile
   // starts koff keys / voff values into the buffer, ti[3] = koff | voff << 8),
   // so that tiles of segments at any offset (recursion levels) still use TMA
-  template <bool DEFER = false, bool SUP = false>
+  // element offset and length of tile t (local index lt) of segment s in
+  // pass j: consecutive TILE-key pieces of the segment, or (FRM == 2) the
+  // Fast Radix tile table over the estimated layout
+  template <int FRM = 0>
+  static __device__ __forceinline__ void tile_loc(const Params<K>& P, const Seg& s, uint32_t t,
+                                                  uint32_t lt, uint32_t& off, uint32_t& cnt) {
+    if (FRM == 2) {
+      const uint2 e = P.fr_tab[t];
+      off = e.x;
+      cnt = e.y;
+    } else {
+      off = s.start + lt * TILE;
+      cnt = min((uint32_t)TILE, s.len - lt * TILE);
+    }
+  }
+
+  template <bool DEFER = false, bool SUP = false, int FRM = 0>
   static __device__ __forceinline__ void claim_tile(const Params<K>& P, int j, const Seg* q,
                                                     uint32_t nseg, uint32_t total, uint32_t* ti,
                                                     K* kb, V* vb, unsigned long long* bar) {
@@ -681,14 +733,16 @@ struct Phases {
     ti[0] = t;
     ti[2] = 0;
     if (t >= total) return;
-    const uint32_t si = upper_index(nseg, t, [&](uint32_t i) { return q[i].tile0; });
+    const uint32_t si = FRM == 2 ? 0u : upper_index(nseg, t, [&](uint32_t i) { return q[i].tile0; });
     ti[1] = si;
     const Seg& s = q[si];
     const uint32_t lt = t - s.tile0;
-    if (!pass_active(s, j) || s.len - lt * TILE < (uint32_t)TILE) return;
+    uint32_t off, tcnt;
+    tile_loc<FRM>(P, s, t, lt, off, tcnt);
+    if (!pass_active(s, j) || tcnt < (uint32_t)TILE) return;
     const uint32_t sb = route_src(s, j);
-    const K* src = P.kbuf(sb) + s.start + lt * TILE;
-    const V* srcv = PAIRS ? P.vbuf(sb) + s.start + lt * TILE : nullptr;
+    const K* src = P.kbuf(sb) + off;
+    const V* srcv = PAIRS ? P.vbuf(sb) + off : nullptr;
     const bool aligned = !(reinterpret_cast<uintptr_t>(src) & 15) &&
                          !(PAIRS && (reinterpret_cast<uintptr_t>(srcv) & 15));
     if (SUP) ti[3] = 0;
@@ -709,13 +763,13 @@ struct Phases {
       return;
     }
     ti[2] = 1;
-    if (!DEFER) issue_tile<SUP>(P, j, q, ti, kb, vb, bar);
+    if (!DEFER) issue_tile<SUP, FRM>(P, j, q, ti, kb, vb, bar);
   }
   static __device__ __forceinline__ uint32_t sup_bytes(uintptr_t head, uint32_t bytes) {
     return (uint32_t)((head + bytes + 15) & ~(uintptr_t)15);
   }
   // thread 0: start the TMA bulk copy of the claimed tile in ti (ti[2] = 1)
-  template <bool SUP = false>
+  template <bool SUP = false, int FRM = 0>
   static __device__ __forceinline__ void issue_tile(const Params<K>& P, int j, const Seg* q,
                                                     const uint32_t* ti, K* kb, V* vb,
                                                     unsigned long long* bar) {
@@ -723,8 +777,10 @@ struct Phases {
     const Seg& s = q[ti[1]];
     const uint32_t lt = ti[0] - s.tile0;
     const uint32_t sb = route_src(s, j);
-    const K* src = P.kbuf(sb) + s.start + lt * TILE;
-    const V* srcv = PAIRS ? P.vbuf(sb) + s.start + lt * TILE : nullptr;
+    uint32_t off, tcnt;
+    tile_loc<FRM>(P, s, ti[0], lt, off, tcnt);
+    const K* src = P.kbuf(sb) + off;
+    const V* srcv = PAIRS ? P.vbuf(sb) + off : nullptr;
     uint32_t kbytes = TILE * sizeof(K), vbytes = TILE * 4;
     if (SUP && ti[3]) {
       const uint32_t koff = ti[3] & 0xffu, voff = ti[3] >> 8;
@@ -761,11 +817,11 @@ struct Phases {
   // order, which keeps the look-back of later tiles short.
   // FUSEH: the middle pass of a fused level 0 also counts the joint histogram
   // PERM (deal_tile): one tile buffer, refilled once the write-out is done
-  template <int SC_NT, bool FUSEH = false, bool PERM = false>
+  template <int SC_NT, bool FUSEH = false, bool PERM = false, int FRM = 0>
   static __device__ void scatter(const Params<K>& P, int j, uint32_t* sm) {
     constexpr int SC_W = SC_NT / 32;
     Ctl* c = P.ctl;
-    const uint32_t total = c->total_tiles, nseg = c->nseg;
+    const uint32_t total = FRM == 2 ? c->fr_tiles : c->total_tiles, nseg = c->nseg;
     if ((uint32_t)j >= c->max_p) return;  // no segment of this level has pass j
     if (P.fuse && j == 2 && c->level == 0 && *(volatile uint32_t*)&c->fused_ok) return;  // fused pass did it
     const Seg* q = P.segq[c->cur];
@@ -774,6 +830,11 @@ struct Phases {
     uint32_t* s_warp = reinterpret_cast<uint32_t*>(s_dst + 256);  // 16
     uint32_t* ti = s_warp + 16;                                   // 2 x 4 words
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(ti + 8);  // 2, 8-aligned
+    uint32_t* nh = sm + SCATTER_HDR_WORDS - 256;  // Fast Radix: next-digit counters of this CTA
+    if (FRM) {
+      nh[threadIdx.x] = 0;
+      __syncthreads();
+    }
     uint16_t* const perm = reinterpret_cast<uint16_t*>(sm + SCATTER_HDR_WORDS);  // PERM: TILE
     K* const kb0 = PERM ? reinterpret_cast<K*>(perm + TILE)
                         : reinterpret_cast<K*>(sm + SCATTER_HDR_WORDS);  // (1 or 2) x TILE keys
@@ -783,7 +844,7 @@ struct Phases {
       mbar_init(&bar[0], 1);
       mbar_init(&bar[1], 1);
       fence_mbar_init();
-      claim_tile<false, PERM>(P, j, q, nseg, total, ti, kb0, vb0, &bar[0]);
+      claim_tile<false, PERM, FRM>(P, j, q, nseg, total, ti, kb0, vb0, &bar[0]);
     }
     uint32_t phases = 0;  // mbarrier parity per buffer
     // the segment record and its bucket-offset row are re-read only when a
@@ -808,7 +869,7 @@ struct Phases {
       if (si != cur_si) {
         cur_si = si;
         s = q[si];
-        if (threadIdx.x < 256 && pass_active(s, j))
+        if (threadIdx.x < 256 && pass_active(s, j) && FRM != 1)
           bstart = P.hist[(size_t)(s.hist_off + j) * 256 + threadIdx.x];
       }
       const bool tma = ti[cb * 4 + 2] != 0;
@@ -818,8 +879,8 @@ struct Phases {
       auto claim_next = [&]() {
         if (threadIdx.x == 0) {
           const int nb = PERM ? 0 : (cb ^ 1);
-          claim_tile<false, PERM>(P, j, q, nseg, total, ti + nb * 4, kb0 + nb * TILE, vb0 + nb * TILE,
-                                  &bar[nb]);
+          claim_tile<false, PERM, FRM>(P, j, q, nseg, total, ti + nb * 4, kb0 + nb * TILE,
+                                       vb0 + nb * TILE, &bar[nb]);
         }
       };
       // claim the next tile once this one's prefix is known (tickets in
@@ -828,7 +889,7 @@ struct Phases {
         if (!PERM)
           claim_next();
         else if (threadIdx.x == 0)
-          claim_tile<true, true>(P, j, q, nseg, total, ti, kb0, vb0, &bar[0]);
+          claim_tile<true, true, FRM>(P, j, q, nseg, total, ti, kb0, vb0, &bar[0]);
       };
       if (!pass_active(s, j)) {
         claim_next();
@@ -836,8 +897,8 @@ struct Phases {
         continue;
       }
       const uint32_t lt = t - s.tile0;
-      const uint32_t base = s.start + lt * TILE;
-      const uint32_t cnt = min((uint32_t)TILE, s.len - lt * TILE);
+      uint32_t base, cnt;
+      tile_loc<FRM>(P, s, t, lt, base, cnt);
       const uint32_t sb = route_src(s, j), db = route_dst(s, j);
       const K* src = P.kbuf(sb);
       K* dst = P.kbuf(db);
@@ -854,17 +915,19 @@ struct Phases {
         __syncthreads();
       }
       if (cnt == (uint32_t)TILE)
-        deal_tile<SC_NT, true, FUSEH, PERM>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist,
-                                            s_dst, s_warp, dst, dstv, bstart, perm, sup);
+        deal_tile<SC_NT, true, FUSEH, PERM, FRM>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist,
+                                                 s_dst, s_warp, dst, dstv, bstart, perm, sup,
+                                                 smem_u32(nh));
       else
-        deal_tile<SC_NT, false, FUSEH, PERM>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist,
-                                             s_dst, s_warp, dst, dstv, bstart, perm, sup);
+        deal_tile<SC_NT, false, FUSEH, PERM, FRM>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist,
+                                                  s_dst, s_warp, dst, dstv, bstart, perm, sup,
+                                                  smem_u32(nh));
       if (PERM) {  // single buffer: refill it once every thread is done with the write-out
         for (int e = threadIdx.x; e < (SC_W + 1) * 256; e += SC_NT) whist[e] = 0;
         __syncthreads();
         if (threadIdx.x == 0) {
           fence_proxy_async();
-          issue_tile<PERM>(P, j, q, ti, kb0, vb0, &bar[0]);
+          issue_tile<PERM, FRM>(P, j, q, ti, kb0, vb0, &bar[0]);
         }
       }
       fence_proxy_async();  // generic smem accesses before a later TMA into this buffer
@@ -874,6 +937,81 @@ struct Phases {
     if (threadIdx.x == 0) {
       mbar_inval(&bar[0]);
       mbar_inval(&bar[1]);
+    }
+    if (FRM) {  // this CTA's next-digit counts (Fast Radix)
+      __syncthreads();
+      const uint32_t v = nh[threadIdx.x];
+      if (v) atomicAdd(&P.fr_cnt[(FRM == 2 ? 256 : 0) + threadIdx.x], v);
+    }
+  }
+
+  // ------------------------------------------------------- Fast Radix
+  // Fast Radix estimation at level 0 (dfr_config.fast_radix; Alg. 3,
+  // P:211-246, applied to the top call's group of p = 3 digits lo, mid, hi):
+  //   pass lo   deals A into ESTIMATED buckets (capacity ceil(n/256)) in
+  //             C, overflow into chunks after the main regions (FRM = 1), and
+  //             counts digit mid -- no histogram read of the input
+  //   pass mid  reads C bucket by bucket (main region, then its chunks: the
+  //             stable bucket order) through a tile table and deals
+  //             into exact buckets of B (FRM = 2), counting digit hi (Alg. 3
+  //             l.5-6: the top digit counted in the penultimate pass) and the
+  //             joint histogram of the fused pass
+  //   pass hi   the fused last pass (one chain: no chain histogram) B -> A
+  // No pass is skipped (no histogram tells which digits are constant).
+
+  // grid: the level-0 segment's route and flags, zeroed status rows, chunk
+  // table, counters and the fused pass's joint histogram
+  static __device__ void fr_prep(const Params<K>& P) {
+    Ctl* c = P.ctl;
+    const uint32_t gid = blockIdx.x * blockDim.x + threadIdx.x, gsz = gridDim.x * blockDim.x;
+    if (gid == 0) {
+      Seg* q = P.segq[c->cur];
+      Seg s = q[0];
+      s.flags = 0;
+      s.route = (0u | 2u << 2) | (2u | 1u << 2) << 4 | (1u | 2u << 2) << 8;  // A->C, C->B, B->C
+      s.final_buf = 2;
+      s.diff = ~0ull;  // unknown: every lower digit may vary
+      q[0] = s;
+      c->level0_p = s.p;
+      c->level0_run = s.p;
+      c->fr_next_chunk = 0;
+      c->fr_tiles = 0;
+      c->fr_overflow = 0;
+    }
+    for (size_t x = gid; x < 3 * P.status_stride; x += gsz) P.status[x] = 0;
+    for (size_t x = gid; x < (size_t)256 * P.fr_kmax; x += gsz) P.fr_ct[x] = 0;
+    for (uint32_t x = gid; x < 512u; x += gsz) P.fr_cnt[x] = 0;
+    for (uint32_t x = gid; x < 65536u; x += gsz) P.H[x] = 0;
+  }
+
+  // one CTA of 256 threads after pass lo: bucket d's count is pass lo's
+  // inclusive prefix of its last tile; the table of pass mid's tiles (each
+  // bucket's main region in TILE pieces, then its overflow chunks) and pass
+  // mid's exact bucket offsets (from the mid-digit counts pass lo took)
+  static __device__ void fr_plan(const Params<K>& P) {
+    Ctl* c = P.ctl;
+    __shared__ uint32_t s_warp[WARPS];
+    const Seg s = P.segq[c->cur][0];
+    const uint32_t d = threadIdx.x;
+    const uint32_t total = P.status[(size_t)(s.ntiles - 1) * 256 + d] & VAL_MASK;
+    const uint32_t cap = P.fr_cap;
+    const uint32_t main = min(total, cap), ovf = total - main;
+    const uint32_t nmain = (main + TILE - 1) / TILE, novf = (ovf + FR_CHUNK - 1) / FR_CHUNK;
+    uint32_t tt;
+    uint32_t t0 = block_excl_scan(nmain + novf, s_warp, &tt);
+    for (uint32_t k = 0; k < nmain; ++k)
+      P.fr_tab[t0++] = make_uint2(d * cap + k * TILE, min((uint32_t)TILE, main - k * TILE));
+    for (uint32_t k = 0; k < novf; ++k)
+      P.fr_tab[t0++] = make_uint2(256u * cap + (P.fr_ct[(size_t)d * P.fr_kmax + k] - 1u) * FR_CHUNK,
+                                  min(FR_CHUNK, ovf - k * FR_CHUNK));
+    uint32_t tot2;
+    const uint32_t ex = block_excl_scan(P.fr_cnt[d], s_warp, &tot2);
+    P.hist[(size_t)(s.hist_off + 1) * 256 + d] = ex;
+    uint32_t tov;
+    block_excl_scan(ovf, s_warp, &tov);
+    if (d == 0) {
+      c->fr_tiles = tt;
+      c->fr_overflow = tov;
     }
   }
 
@@ -1590,24 +1728,40 @@ struct Phases {
       ntl += s_w2[e];
       gmx = max(gmx, s_m[e]);
     }
+    // Fast Radix mode counts no chain histogram: one chain in s-run order
+    const uint32_t chains = P.fr ? 1u : (uint32_t)F_CHAINS;
     // tiles per chain (2 warps per chain) and this thread's first index in its chain
     uint32_t nch[F_CHAINS];
 #pragma unroll
     for (int ch = 0; ch < F_CHAINS; ++ch) nch[ch] = s_w2[2 * ch] + s_w2[2 * ch + 1];
-    const int ch = t >> 6;
+    const int ch = chains == 1 ? 0 : t >> 6;
     uint32_t jb = b - nz + ((w & 1) ? s_w2[w - 1] : 0u);  // non-empty s-runs before mine in my chain
+    uint32_t pb = 0;
+    for (int e = 0; e < w; ++e) pb += s_w2[e];
+    if (chains == 1) jb = pb + b - nz;  // the global index
     uint32_t nmin = nch[0];
 #pragma unroll
     for (int e = 1; e < F_CHAINS; ++e) nmin = min(nmin, nch[e]);
+    if (chains == 1) nmin = ntl;
     // ticket of the j-th tile of chain ch: round robin over the chains that
-    // still have tiles (while every chain has: F_CHAINS * j + ch)
+    // still have tiles (while every chain has: chains * j + ch)
     auto ticket = [&](uint32_t j) {
-      if (j < nmin) return F_CHAINS * j + (uint32_t)ch;
+      if (j < nmin) return chains * j + (uint32_t)ch;
       uint32_t p = 0;
 #pragma unroll
       for (int e = 0; e < F_CHAINS; ++e) p += min(nch[e], j) + ((e < ch && nch[e] > j) ? 1u : 0u);
       return p;
     };
+    if (P.fr) {  // the top digit's bucket offsets from its counts (taken in the middle pass)
+      __shared__ uint32_t s_c[256];
+      if (t < 256) s_c[t] = P.fr_cnt[256 + t];
+      __syncthreads();
+      if (t < 256) {
+        uint32_t e = 0;
+        for (int x = 0; x < t; ++x) e += s_c[x];
+        P.hist[(size_t)(s.hist_off + 2) * 256 + t] = e;
+      }
+    }
     const bool ok = gmx <= (uint32_t)FT_MAX && tot == s.len;
     if (ok) {
       uint32_t pos = pa + a - sum;
@@ -1628,6 +1782,8 @@ struct Phases {
       c->fused_ok = ok ? 1u : 0u;
       c->fused_tiles = ntl;
       c->fticket = 0;
+      c->fused_regular = chains * nmin;  // tickets below this: chain predecessor = ticket - chains
+      c->fused_chains = chains;
     }
   }
 
@@ -1758,6 +1914,7 @@ struct Phases {
     // complete; the first tile of a chain publishes its inclusive prefix
     // (the chain's base + its count) at once
     const uint32_t* jbase = P.J + 4096;
+    const uint32_t regular = c->fused_regular, chains = c->fused_chains;
     auto publish = [&](uint32_t tt, uint32_t cb, uint32_t prev, uint32_t chn) {
       if (tt < ntiles) {
         const uint4 c4 = reinterpret_cast<const uint4*>(cnt_of(cb))[d];
@@ -1898,22 +2055,49 @@ struct Phases {
         } else {
           excl = 0;
 #ifndef DFR_F_NOLB  // (timing experiment only: wrong output)
-          uint32_t pt = tprev;
-          while (true) {
-            const uint32_t v = ld_relaxed(status + (size_t)pt * 256 + d);
-            if ((v >> 30) == 0) {  // not published yet
+          if (t < regular) {
+            // the regular part of the ticket order: the chain predecessors are
+            // t - chains, t - 2 chains, ...: DFR_LB of them per round trip (the
+            // chain's first tile is inclusive, so the walk stops there)
+            int tt = (int)tprev;
+            while (true) {
+              constexpr int LB = DFR_LB;
+              uint32_t v[LB];
+#pragma unroll
+              for (int i = 0; i < LB; ++i) {
+                const int r = tt - (int)chains * i;
+                v[i] = r >= 0 ? ld_relaxed(status + (size_t)r * 256 + d) : FLAG_INC;
+              }
+              int q = 0;
+              bool done = false;
+#pragma unroll
+              for (; q < LB; ++q) {
+                if ((v[q] >> 30) == 0) break;
+                excl += v[q] & VAL_MASK;
+                if (v[q] & FLAG_INC) {
+                  done = true;
+                  break;
+                }
+              }
+              if (done) break;
 #ifdef DFR_LB_STATS
-              atomicAdd(&g_lb_stats[1], 1ull);
+              atomicAdd(&g_lb_stats[q == 0 ? 1 : 0], 1ull);
 #endif
-              __nanosleep(DFR_LB_SLEEP);
-              continue;
+              if (q == 0) __nanosleep(DFR_LB_SLEEP);
+              tt -= (int)chains * q;
             }
-            excl += v & VAL_MASK;
-            if (v & FLAG_INC) break;
-#ifdef DFR_LB_STATS
-            atomicAdd(&g_lb_stats[0], 1ull);
-#endif
-            pt = P.ftiles[pt].z;
+          } else {  // the tail of the order: follow the chain links
+            uint32_t pt = tprev;
+            while (true) {
+              const uint32_t v = ld_relaxed(status + (size_t)pt * 256 + d);
+              if ((v >> 30) == 0) {  // not published yet
+                __nanosleep(DFR_LB_SLEEP);
+                continue;
+              }
+              excl += v & VAL_MASK;
+              if (v & FLAG_INC) break;
+              pt = P.ftiles[pt].z;
+            }
           }
 #endif
 #ifdef DFR_LB_STATS
