@@ -176,6 +176,14 @@ __global__ void __launch_bounds__(THREADS, 2) k_mid(const __grid_constant__ Para
   pdl_enter();
   Phases<K, PAIRS>::template mid<MID_CAP>(P, sm, len_lo);
 }
+// keys only: the mid buckets, one round per digit (Phases::midf)
+template <class K>
+__global__ void __launch_bounds__(Phases<K, false>::FNT, 3) k_midf(const __grid_constant__ Params<K> P, int round) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  pdl_enter();
+  Phases<K, false>::midf(P, sm, round);
+}
+
 // the mid buckets of at most MID_CAP_S keys, at 4 CTAs/SM
 template <class K, bool PAIRS>
 __global__ void __launch_bounds__(THREADS, 4) k_mid_s(const __grid_constant__ Params<K> P) {
@@ -279,7 +287,7 @@ struct PhaseEv {  // optional caller-provided events around each phase
 struct Dev {
   int sms = 0;
   int occ_hist = 0, occ_scatter = 0, occ_divert = 0, occ_mid = 0, occ_mid_s = 0, occ_levels = 0,
-      occ_fused = 0;
+      occ_fused = 0, occ_midf = 0;
 };
 
 template <class K, bool PAIRS>
@@ -344,6 +352,13 @@ static cudaError_t get_dev(Dev& out) {
                                                             Ph::FNT, Ph::SMEM_FUSED);
     }
     setup((const void*)k_levels<K, PAIRS>, Ph::SMEM_LEVEL, &d.occ_levels);
+    if (err == cudaSuccess && !PAIRS) {  // keys-only mid rounds: FNT-thread CTAs
+      err = cudaFuncSetAttribute((const void*)k_midf<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Ph::SMEM_FUSED);
+      if (err == cudaSuccess)
+        err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_midf, (const void*)k_midf<K>, Ph::FNT,
+                                                            Ph::SMEM_FUSED);
+    }
     devs[dev] = d;
     errs[dev] = err;
   });
@@ -353,8 +368,24 @@ static cudaError_t get_dev(Dev& out) {
 
 static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
+// the buckets N_d < s <= C: keys only, D rounds of k_midf (one digit each);
+// pairs, the shared-memory recursion of k_mid_s / k_mid
+template <class K, bool PAIRS>
+static void launch_mid(const Dev& dv, cudaStream_t st, const Params<K>& P) {
+  using Ph = Phases<K, PAIRS>;
+  if constexpr (!PAIRS) {
+    for (int r = 0; r < (int)sizeof(K); ++r)
+      launch_pdl(k_midf<K>, dv.sms * std::max(1, dv.occ_midf), Ph::FNT, Ph::SMEM_FUSED, st, P, r);
+    g_launches += sizeof(K);
+  } else {
+    launch_pdl(k_mid_s<K, PAIRS>, dv.sms * std::max(1, dv.occ_mid_s), THREADS, Ph::SMEM_MID_S, st, P);
+    launch_pdl(k_mid<K, PAIRS>, dv.sms * std::max(1, dv.occ_mid), THREADS, Ph::SMEM_MID, st, P, MID_CAP_S);
+    g_launches += 2;
+  }
+}
+
 struct Layout {
-  size_t b_keys, b_vals, c_keys, ctl, segq0, segq1, midq, hist, status, fh, ftiles, fj, total;
+  size_t b_keys, b_vals, c_keys, ctl, segq0, segq1, midq, midq2, hist, status, fh, ftiles, fj, total;
   size_t fr_ct, fr_tab, fr_cnt, fr_cap, fr_kmax;
   size_t max_segs, mid_cap, hist_rows, tiles_max;
 };
@@ -389,6 +420,7 @@ static Layout make_layout(size_t n, int kb, int vb, uint32_t n_d, int min_passes
   L.segq0 = take(L.max_segs * sizeof(Seg));
   L.segq1 = take(L.max_segs * sizeof(Seg));
   L.midq = take(L.mid_cap * sizeof(MidE));
+  L.midq2 = take(L.mid_cap * sizeof(MidE));
   L.hist = take(L.hist_rows * 256 * 4);
   int passes = est_top_passes(n, n_d);  // no group of any level has more passes
   passes = passes < min_passes ? min_passes : (passes > MAX_PASSES ? MAX_PASSES : passes);
@@ -419,6 +451,7 @@ static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals,
   P.segq[0] = reinterpret_cast<Seg*>(ws + L.segq0);
   P.segq[1] = reinterpret_cast<Seg*>(ws + L.segq1);
   P.midq = reinterpret_cast<MidE*>(ws + L.midq);
+  P.midq2 = reinterpret_cast<MidE*>(ws + L.midq2);
   P.hist = reinterpret_cast<uint32_t*>(ws + L.hist);
   P.status = reinterpret_cast<uint32_t*>(ws + L.status) + LB_PAD * 256;
   P.status_stride = L.tiles_max * 256;
@@ -522,10 +555,9 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
       return DFR_ERR_CUDA;
     }
     pe.begin(DFR_PHASE_MID);
-    launch_pdl(k_mid_s<K, PAIRS>, sms * std::max(1, dv.occ_mid_s), THREADS, Ph::SMEM_MID_S, st, P);
-    launch_pdl(k_mid<K, PAIRS>, sms * std::max(1, dv.occ_mid), THREADS, Ph::SMEM_MID, st, P, MID_CAP_S);
+    launch_mid<K, PAIRS>(dv, st, P);
     pe.end(DFR_PHASE_MID);
-    g_launches += 4;
+    g_launches += 2;
   } else if (n <= (size_t)MID_CAP) {  // the whole input fits one on-chip DFR
     for (int i = 0; i < DFR_PHASE_MID; ++i) pe.skip(i);
     pe.begin(DFR_PHASE_MID);
@@ -605,11 +637,9 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
       return DFR_ERR_CUDA;
     }
     pe.begin(DFR_PHASE_MID);
-    const int g_mid = sms * std::max(1, dv.occ_mid);
-    launch_pdl(k_mid_s<K, PAIRS>, sms * std::max(1, dv.occ_mid_s), THREADS, Ph::SMEM_MID_S, st, P);
-    launch_pdl(k_mid<K, PAIRS>, g_mid, THREADS, Ph::SMEM_MID, st, P, MID_CAP_S);
+    launch_mid<K, PAIRS>(dv, st, P);
     pe.end(DFR_PHASE_MID);
-    g_launches += 7 + p0;
+    g_launches += 5 + p0;
   }
   cudaError_t e = cudaGetLastError();
   int rc = (e == cudaSuccess) ? DFR_OK : DFR_ERR_CUDA;

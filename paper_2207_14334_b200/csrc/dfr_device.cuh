@@ -139,6 +139,7 @@ struct Ctl {
   uint32_t fr_next_chunk;       // Fast Radix: overflow chunks handed out so far
   uint32_t fr_tiles;            // Fast Radix: tiles of the pass that reads the estimated layout
   uint32_t fr_overflow;         // Fast Radix: records the estimated pass dealt to overflow
+  uint32_t mround[12];          // keys-only mid rounds: [r + 1] buckets queued for round r + 1
 };
 
 template <class K>
@@ -152,6 +153,7 @@ struct Params {
   Ctl* ctl;
   Seg* segq[2];
   MidE* midq;
+  MidE* midq2;          // keys-only mid rounds: the queue of the odd rounds (capacity mid_cap)
   uint32_t* hist;       // histogram / bucket-offset rows, 256 u32 each
   uint32_t* status;     // look-back status words [MAX_PASSES][tiles_max][256]
   size_t status_stride; // words per pass

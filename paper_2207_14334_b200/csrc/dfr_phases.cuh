@@ -2172,6 +2172,256 @@ struct Phases {
 #endif
   }
 
+  // --------------------------------------------------------- mid (fast)
+  // Keys-only buckets N_d < len <= C (Alg. 4 l.11 "recurse on the large
+  // bucket"), one bucket per CTA iteration, in rounds.  Round r takes the
+  // buckets queued for it and runs Alg. 4 on each with p' = 1 (est(len) = 1
+  // for len <= N_d * 256): a deal on its highest non-constant digit hi, split
+  // by 2 more bits into sub-buckets as in the fused pass, and every digit
+  // bucket of <= N_d keys sorted on the spot (ranks by 16-bit composites,
+  // ties re-ranked exactly), the keys written straight to their final place
+  // in A.  A digit bucket > N_d is written in slot order and queued for round
+  // r + 1 with the next digit (its keys are all in A by then); digits exhausted
+  // (hi < 0, or a digit-0 bucket) means equal keys: nothing to sort.
+  // (Pairs keep the shared-memory recursion of mid(): stability needs the
+  // input order inside a bucket.)
+  static __device__ void midf(const Params<K>& P, uint32_t* sm, int round) {
+    constexpr bool WIDE = sizeof(K) == 8;
+    Ctl* c = P.ctl;
+    const MidE* q = (round & 1) ? P.midq2 : P.midq;
+    MidE* nq = (round & 1) ? P.midq : P.midq2;
+    const uint32_t total = min(round == 0 ? c->mid_count : c->mround[round], P.mid_cap);
+    if (total == 0) return;
+    uint32_t* nqc = &c->mround[round + 1];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t nd = P.n_d;
+    char* base = reinterpret_cast<char*>(sm);
+    uint32_t* bdesc = reinterpret_cast<uint32_t*>(base + FS::BDESC);
+    uint32_t* flag = reinterpret_cast<uint32_t*>(base + FS::FLAG);
+    uint32_t* s_warp = reinterpret_cast<uint32_t*>(base + FS::WARP);
+    uint32_t* misc = reinterpret_cast<uint32_t*>(base + FS::MISC);
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(base + FS::CNT);
+    const uint32_t keys_a = smem_u32(base + FS::KEYS), cmp_a = smem_u32(base + FS::CMP),
+                   cnt_a = smem_u32(cnt);
+    const uint32_t d = threadIdx.x;
+    const uint32_t kofs = w * 32 * FKPT + lane;
+    reinterpret_cast<uint4*>(cnt)[d] = make_uint4(0, 0, 0, 0);
+    if (d < FNS / 32) flag[d] = 0;
+    if (d == 0) {
+      misc[5] = 0;
+      *reinterpret_cast<unsigned long long*>(misc + 6) = 0ull;
+    }
+    __syncthreads();
+    // the keys of the next bucket are loaded while this one is ranked
+    K key[FKPT];
+    auto load = [&](const MidE& m) {
+      if (m.hi < 0) return;  // (copied, not loaded)
+      const K* p = P.kbuf(m.buf) + m.start + kofs;
+      const int lim = (int)m.len - (int)kofs;
+#pragma unroll
+      for (int i = 0; i < FKPT; ++i) key[i] = i * 32 < lim ? p[i * 32] : K(0);
+    };
+    uint32_t e = blockIdx.x;
+    MidE me = {0, 0, -1, 0};
+    if (e < total) {
+      me = q[e];
+      load(me);
+    }
+    for (; e < total;) {
+      const uint32_t en = e + gridDim.x;
+      MidE mn = {0, 0, -1, 0};
+      if (en < total) mn = q[en];
+      const uint32_t len = me.len;
+      const K* X = P.kbuf(me.buf) + me.start;
+      K* const out = P.A + me.start;
+      auto advance = [&]() {
+        e = en;
+        me = mn;
+        load(me);
+      };
+      if (me.hi < 0) {  // digits exhausted: equal keys, sorted (Alg. 2 l.17-18)
+        if (me.buf) coop_copy(out, X, len, threadIdx.x, THREADS);
+        advance();
+        continue;
+      }
+      // the bucket's highest non-constant digit (OR of k ^ k0)
+      {
+        const int lim = (int)len - (int)kofs;
+        const K k0 = X[0];
+#pragma unroll
+        for (int m = 0; m < FKPT; ++m)
+          if (!(m * 32 < lim)) key[m] = k0;
+        K acc = 0;
+#pragma unroll
+        for (int m = 0; m < FKPT; ++m) acc |= key[m] ^ k0;
+        unsigned long long a = (unsigned long long)acc;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) a |= __shfl_xor_sync(0xffffffffu, a, o);
+        if (lane == 0 && a) atomicOr(reinterpret_cast<unsigned long long*>(misc + 6), a);
+      }
+      __syncthreads();
+      const unsigned long long bdiff = *reinterpret_cast<volatile unsigned long long*>(misc + 6);
+      const int dg = highest_nonconst(bdiff, me.hi);
+      __syncthreads();  // every thread has read it
+      if (d == 0) *reinterpret_cast<unsigned long long*>(misc + 6) = 0ull;
+      if (dg < 0) {  // all keys equal: sorted (Alg. 2 l.17-18)
+        if (me.buf) coop_copy(out, X, len, threadIdx.x, THREADS);
+        advance();
+        continue;
+      }
+      const int sbs = 8 * dg - FSB;  // sub-bucket bits (dg >= 1); below them R = sbs bits
+      auto sub_of = [&](K k) -> uint32_t {
+        return digit_of(k, dg) << FSB | (dg ? ((uint32_t)(k >> sbs) & ((1u << FSB) - 1)) : 0u);
+      };
+      // 16-bit composite of the bits below the sub-bucket bits: exact (the R
+      // bits and the slot) when they fit 14 bits, else the top 16 of them
+      // scaled onto the normal fp16 values (ties re-ranked exactly)
+      const bool exact = sbs + 8 <= 14;
+      auto comp_of = [&](K k, uint32_t slot) -> uint32_t {
+        if (exact) return 0x0400u + (((uint32_t)k & ((1u << sbs) - 1)) << 8 | slot);
+        const uint32_t v16 = sbs >= 16 ? (uint32_t)(k >> (sbs - 16)) & 0xffffu
+                                       : ((uint32_t)k << (16 - sbs)) & 0xffffu;
+        const uint32_t v = (v16 * 61440u) >> 16;
+        return v < 30720u ? (0x8000u | (0x0400u + 30719u - v)) : (0x0400u + v - 30720u);
+      };
+      (void)WIDE;
+      // ---- sub-bucket and slot of every key
+      uint32_t ds[FKPT];
+      {
+        const int lim = (int)len - (int)kofs;
+#pragma unroll
+        for (int m = 0; m < FKPT; ++m) {
+          ds[m] = ~0u;
+          if (m * 32 < lim) {
+            const uint32_t sb = sub_of(key[m]);
+            uint32_t slot;
+            asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(slot) : "r"(cnt_a + 4 * sb) : "memory");
+            ds[m] = sb | slot << 10;
+          }
+        }
+      }
+      __syncthreads();
+      // ---- layout (thread d: digit value d and its sub-buckets)
+      const uint4 c4 = reinterpret_cast<const uint4*>(cnt)[d];
+      const uint32_t cs[4] = {c4.x, c4.y, c4.z, c4.w};
+      const uint32_t cd = c4.x + c4.y + c4.z + c4.w;
+      const bool small = cd <= nd && dg > 0;  // a digit-0 bucket holds equal keys
+      uint32_t padc = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) padc += (small && cs[r] >= 2) ? (cs[r] + 3) & ~3u : 0u;
+      const uint32_t ex = fused_scan(cd | padc << 16, s_warp);
+      const uint32_t lst = ex & 0xffffu;
+      {
+        uint32_t so = lst, co = ex >> 16;
+        uint32_t bd[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint32_t ng = (small && cs[r] >= 2) ? (cs[r] + 3) >> 2 : 0u;
+          bd[r] = (co >> 2) | ng << 11 | so << 18;
+          if (ng) sts64(cmp_a + 2 * (co + 4 * ng - 4), 0x7c007c007c007c00ull);
+          so += cs[r];
+          co += 4 * ng;
+        }
+        reinterpret_cast<uint4*>(bdesc)[d] = make_uint4(bd[0], bd[1], bd[2], bd[3]);
+      }
+      if (cd > nd && dg > 0) {  // a large digit bucket: the next round, next digit (Alg. 4 l.11)
+        const uint32_t idx = atomicAdd(nqc, 1u);
+        if (idx < P.mid_cap) {
+          MidE m;
+          m.start = me.start + lst;
+          m.len = (uint16_t)cd;
+          m.hi = (int8_t)(dg - 1);
+          m.buf = 0;
+          nq[idx] = m;
+        } else {
+          flag_overflow(c, 64u);
+        }
+      }
+      __syncthreads();
+      // ---- keys grouped by sub-bucket, composites of the small ones
+#pragma unroll
+      for (int m = 0; m < FKPT; ++m) {
+        if (ds[m] != ~0u) {
+          const uint32_t slot = ds[m] >> 10;
+          const uint32_t bd = bdesc[ds[m] & (FNS - 1)];
+          const uint32_t x = (bd >> 18) + slot;
+          if constexpr (sizeof(K) == 8)
+            sts64(keys_a + 8 * x, (unsigned long long)key[m]);
+          else
+            sts32(keys_a + 4 * x, (uint32_t)key[m]);
+          if ((bd >> 11) & 127u) sts16(cmp_a + 2 * (4 * (bd & 2047u) + slot), comp_of(key[m], slot));
+        }
+      }
+      const uint32_t e_cur = e;
+      (void)e_cur;
+      advance();  // the next bucket's keys in flight during the ranks
+      __syncthreads();
+      // ---- slot-major ranks; every key to its final place
+      int dev = 0;
+      for (uint32_t x = threadIdx.x; x < len; x += FNT) {
+        const K k = ldsk<K>(keys_a + sizeof(K) * x);
+        const uint32_t bd = bdesc[sub_of(k)];
+        const uint32_t ng = (bd >> 11) & 127u;
+        uint32_t pos = x;
+        if (ng) {
+          const uint32_t bl = bd >> 18;
+          const uint32_t pa = cmp_a + 8 * (bd & 2047u);
+          const __half2 me2 = __ushort_as_half2_pair(lds16(pa + 2 * (x - bl)));
+          __half2 acc = __float2half2_rn(0.f);
+          for (uint32_t g = 0; g < ng; ++g) {
+            const uint2 v = lds64v(pa + 8 * g);
+            acc = __hadd2(acc, __hlt2(u2h2(v.x), me2));
+            acc = __hadd2(acc, __hlt2(u2h2(v.y), me2));
+          }
+          pos = bl + (uint32_t)__half2ushort_rz(__hadd(__low2half(acc), __high2half(acc)));
+          dev += (int)pos - (int)x;
+        }
+        out[pos] = k;
+      }
+      if (!exact) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) dev += __shfl_xor_sync(0xffffffffu, dev, o);
+        if (lane == 0 && dev) atomicAdd(reinterpret_cast<int*>(misc + 5), dev);
+      }
+      __syncthreads();
+      const int tie_sum = *reinterpret_cast<volatile int*>(misc + 5);
+      __syncthreads();  // every thread has read it
+      if (d == 0) misc[5] = 0;
+      if (!exact && tie_sum != 0) {  // (rare) tied composites: re-rank those sub-buckets exactly
+        uint32_t bad = 0;
+        {
+          const uint4 b4 = reinterpret_cast<const uint4*>(bdesc)[d];
+          const uint32_t bds[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (small && cs[r] >= 2) {
+              const uint32_t ca = cmp_a + 8 * (bds[r] & 2047u);
+              bool eq = false;
+              for (uint32_t y = 0; y + 1 < cs[r]; ++y) {
+                const uint32_t a = lds16(ca + 2 * y);
+                for (uint32_t z = y + 1; z < cs[r]; ++z) eq |= lds16(ca + 2 * z) == a;
+              }
+              bad |= (uint32_t)eq << r;
+            }
+        }
+        if (bad) atomicOr(&flag[d >> 3], bad << (4 * (d & 7)));
+        __syncthreads();
+        for (uint32_t fw = w; fw < FNS / 32; fw += FNW) {
+          uint32_t bits = flag[fw];
+          while (bits) {
+            const uint32_t sb = fw * 32 + __ffs(bits) - 1;
+            bits &= bits - 1;
+            fused_fix(keys_a, bdesc[sb] >> 18, cnt[sb], out);
+          }
+        }
+        __syncthreads();
+        if (d < FNS / 32) flag[d] = 0;
+      }
+      reinterpret_cast<uint4*>(cnt)[d] = make_uint4(0, 0, 0, 0);
+      __syncthreads();
+    }
+  }
+
   // ------------------------------------------------------------------ mid
   // stable counting pass over smem range [lo, lo+L) on digit g: a -> b
   template <int MK>  // keys per thread: L <= THREADS * MK
