@@ -338,32 +338,49 @@ def run_dfr(args, rank, world, local_rank):
     ms_per_step = elapsed / K
     peak, peak_src = peak_hbm()
 
-    # roofline of the dominant kernel (the stable deal, k_scatter)
-    smax = max(phase_ms.get(f"scatter{j}", 0.0) for j in range(4))
-    sc = [phase_ms[f"scatter{j}"] for j in range(4)
-          if smax > 0 and phase_ms[f"scatter{j}"] > 0.05 * smax]
-    dominant = max(phase_ms, key=lambda k: phase_ms[k]) if phase_ms else None
-    pass_bytes = n * 2 * (kb + vb)
-    sc_ms = statistics.mean(sc) if sc else None
-    achieved = pass_bytes / (sc_ms / 1e3) / 1e9 if sc_ms else None
+    # roofline of the dominant kernel: the phase with the largest
+    # device time per sort; its algorithmic bytes per launch = its per-key bytes
+    # x n.  Phases (dfr.h DFR_PHASE_*): hist = one read of the keys (kb); a deal
+    # (scatter0/1, and scatter2 = the fused last deal + diversion on the fused
+    # path, or the plain last deal) reads and writes each record (2(kb+vb));
+    # divert = read + write of the records it sorts (2(kb+vb)).
+    per_key = {"hist": kb, "scatter0": 2 * (kb + vb), "scatter1": 2 * (kb + vb),
+               "scatter2": 2 * (kb + vb), "scatter3": 2 * (kb + vb), "divert": 2 * (kb + vb)}
+    cand = {k: v for k, v in phase_ms.items() if k in per_key and v > 0.05}
+    dominant = max(cand, key=lambda k: cand[k]) if cand else None
+    fused_path = phase_ms.get("divert", 0.0) < 0.05 and phase_ms.get("scatter2", 0.0) > 0.05
+    kname = {"hist": "k_hist (one read: the group digits' histograms)",
+             "scatter0": "k_scatter (stable deal, lowest group digit)",
+             "scatter1": "k_scatter_fh (stable deal, middle digit + joint histogram)",
+             "scatter2": ("k_fused (last deal + diversion of its small buckets, one kernel)"
+                          if fused_path else "k_scatter (stable deal, top group digit)"),
+             "divert": "k_divert (scan for large buckets + small-bucket sort)"}.get(dominant, dominant)
+    dom_ms = cand.get(dominant)
+    dom_bytes = n * per_key[dominant] if dominant else None
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms else None
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
-        traffic = tj.get(f"{args.case}:{n}:k_scatter")
+        traffic = tj.get(f"{args.case}:{n}:{'k_fused' if dominant == 'scatter2' and fused_path else 'k_scatter'}")
     except Exception:
         pass
-    roofline = {"bound": "hbm", "kernel": "k_scatter (one stable deal)", "achieved": achieved,
-                "peak": peak, "unit": "GB/s", "frac": achieved / peak if achieved else None,
-                "traffic": traffic, "algorithmic_bytes_per_launch": pass_bytes,
-                "avg_launch_ms": sc_ms, "launches_per_step": len(sc), "peak_source": peak_src,
-                "largest_phase": dominant}
-    sort_bytes = n * (SORT_BYTES_PER_KEY_U64 if kb == 8 else 0)
+    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None, "traffic": traffic,
+                "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
+                "peak_source": peak_src,
+                "timing": "CUDA events the library records around each phase on the sort's stream, "
+                          "in a separate run of K steps (phase_ms)"}
+    # the whole sort against the bytes the executed path moves (fused path:
+    # 8 histogram + 3 x 16 deals = 56 B/key for u64 keys; plain path: + 16 of
+    # the diversion = 72, SURVEY §8(d)'s plan)
     sort_roof = None
-    if kb == 8 and not c.pairs:
-        gbs = sort_bytes / (ms_per_step / 1e3) / 1e9 / 1.0
-        sort_roof = {"bytes_per_key": SORT_BYTES_PER_KEY_U64, "achieved_GBps": gbs,
-                     "frac_of_measured_copy": gbs / peak, "frac_of_8TBps": gbs / NOMINAL_HBM_GBS}
+    if not c.pairs:
+        bpk = kb + 3 * 2 * kb + (0 if fused_path else 2 * kb)
+        gbs = n * bpk / (ms_per_step / 1e3) / 1e9
+        sort_roof = {"bytes_per_key": bpk, "achieved_GBps": gbs, "frac_of_measured_copy": gbs / peak,
+                     "frac_of_8TBps": gbs / NOMINAL_HBM_GBS,
+                     "survey_plan_72B_equiv_frac_of_8TBps": n * 9 * kb / (ms_per_step / 1e3) / 1e9 / NOMINAL_HBM_GBS}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",

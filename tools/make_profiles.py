@@ -20,15 +20,16 @@ for r in rows[hi + 1:]:
     if len(r) != len(h): continue
     k = (r[ix["ID"]], r[ix["Kernel Name"]])
     per.setdefault(k, {})[r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", ""))
-sc = [v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for (i, n), v in per.items()
-      if "k_scatter" in n and v["gpu__time_duration.sum"] > 100000]
 bench = json.load(open(os.path.join(go, f"{tag}_bench.json")))
 n = bench["config"]["n"]; case = bench["config"]["workload"].split(":")[0]
 tj_path = os.path.join(pr, "traffic.json")
 tj = json.load(open(tj_path)) if os.path.exists(tj_path) else {}
-if sc:
-    tj[f"{case}:{n}:k_scatter"] = sum(sc) / len(sc)
-    json.dump(tj, open(tj_path, "w"), indent=1)
+for fam in ["k_scatter<", "k_scatter_fh", "k_fused", "k_hist"]:
+    sc = [v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for (i, nm), v in per.items()
+          if fam in nm and v["gpu__time_duration.sum"] > 100000]
+    if sc:
+        tj[f"{case}:{n}:{fam.rstrip('<')}"] = sum(sc) / len(sc)
+json.dump(tj, open(tj_path, "w"), indent=1)
 # full-capture summary
 rep = os.path.join(go, f"{tag}_full.ncu-rep")
 out = []
@@ -59,7 +60,7 @@ if os.path.exists(rep):
             if w in hh:
                 i = hh.index(w)
                 out.append(f"  {w:62s} {r[i]} {uu[i]}")
-    for k in ("k_hist", "k_scatter", "k_divert"):
+    for k in ("k_hist", "k_scatter", "k_scatter_fh", "k_fused"):
         s = subprocess.run([sys.executable, os.path.join(root, "tools", "ncu_regions.py"), rep, k],
                            capture_output=True, text=True).stdout.split("\n")[:2]
         out.append(f"==== stall mix {k}: " + " | ".join(s))
