@@ -60,6 +60,8 @@ def parse():
                     help="phases timed with CUDA events inside the HEADLINE timed region (events "
                          "between kernels stop programmatic dependent launch from overlapping "
                          "them); the per-phase times always come from a separate run of K steps")
+    ap.add_argument("--stable-deals", action="store_true",
+                    help="dfr_config.stable_deals = 1 (every deal the stable ballot multi-split)")
     ap.add_argument("--no-cold", action="store_true", help="skip the cold-pool trial")
     ap.add_argument("--fast-radix", action="store_true",
                     help="dfr_config.fast_radix = 1 (Fast Radix estimation of the first group pass)")
@@ -251,6 +253,8 @@ def run_dfr(args, rank, world, local_rank):
         b = bufs[i % nbuf]
         vbuf = vbufs[i % nbuf]
         kw = {"fast_radix": True} if args.fast_radix else {}
+        if args.stable_deals:
+            kw["stable_deals"] = True
         dfr.sort(b, vbuf, events=ev, fused=None if args.fused == "auto" else False, **kw)
 
     def restore_buf(i):

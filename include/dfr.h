@@ -91,6 +91,15 @@ typedef struct dfr_config {
                                bucket and counts the top digit (the top digit counted in the
                                penultimate pass, Alg. 3 l.5-6).  No pass is skipped.
                                Same output. */
+  uint32_t stable_deals;    /* 0 (default): keys-only sorts rank the keys of equal digit in
+                               any order inside a deal tile that is constant in the group
+                               digits below the dealt one (always true for the group's
+                               lowest digit) — shared-memory atomics instead of the stable
+                               ballot multi-split.  Same output: equal keys are
+                               indistinguishable, the group's later passes are stable and
+                               every bucket is then sorted on all lower digits (DESIGN.md
+                               R5).  1: every deal is the stable counting pass of P:118-120.
+                               Pairs always deal stably.  Other values: DFR_ERR_INVALID. */
 } dfr_config;
 
 /* Phases timed through dfr_config.phase_events. */

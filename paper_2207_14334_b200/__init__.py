@@ -44,7 +44,7 @@ class Config(ctypes.Structure):
     _fields_ = [("n_d", ctypes.c_uint32), ("skip_trivial_passes", ctypes.c_uint32),
                 ("phase_events", ctypes.POINTER(ctypes.c_void_p)),
                 ("fused_last_pass", ctypes.c_uint32), ("full_lsd", ctypes.c_uint32),
-                ("fast_radix", ctypes.c_uint32)]
+                ("fast_radix", ctypes.c_uint32), ("stable_deals", ctypes.c_uint32)]
 
 
 class Stats(ctypes.Structure):
@@ -128,14 +128,15 @@ def _dev_tensor(t, widths):
     return t
 
 
-def _cfg(n_d, skip_trivial, events=None, fused=None, full_lsd=False, fast_radix=False):
+def _cfg(n_d, skip_trivial, events=None, fused=None, full_lsd=False, fast_radix=False,
+         stable_deals=False):
     """events: None or a sequence of 2*len(PHASES) torch.cuda.Event(enable_timing=True)
     (None entries: that phase is not timed).
     fused: None (default: the fused last deal + diversion where eligible, dfr.h),
     True (same, explicit) or False (always the separate deal and diversion)."""
     mode = 0 if fused is None else (1 if fused else 2)
     c = Config(int(n_d), 1 if skip_trivial else 0, None, mode, 1 if full_lsd else 0,
-               1 if fast_radix else 0)
+               1 if fast_radix else 0, 1 if stable_deals else 0)
     if events is not None:
         arr = (ctypes.c_void_p * len(events))(*[int(e.cuda_event) if e is not None else 0
                                                   for e in events])
@@ -149,28 +150,29 @@ def launch_counter() -> int:
 
 
 def sort_u32(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, events=None,
-             fused=None, full_lsd=False, fast_radix=False):
+             fused=None, full_lsd=False, fast_radix=False, stable_deals=False):
     """In-place ascending sort of a contiguous CUDA tensor of 32-bit keys (bit
     patterns read as uint32)."""
     _dev_tensor(keys, (4,))
     st = Stats() if stats else None
     rc = lib().dfr_sort_u32_ex(keys.data_ptr(), keys.numel(), _stream(stream),
                                ctypes.byref(_cfg(n_d, skip_trivial, events, fused, full_lsd,
-                                                 fast_radix)),
+                                                 fast_radix, stable_deals)),
                                ctypes.byref(st) if st is not None else None)
     _check(rc, "dfr_sort_u32")
     return st.as_dict() if st is not None else None
 
 
 def sort_u64(keys, *, n_d=64, skip_trivial=True, stream=None, stats=False, events=None,
-             fused=None, fast_radix=False):
+             fused=None, fast_radix=False, stable_deals=False):
     """In-place ascending sort of a contiguous CUDA tensor of 64-bit keys (bit
     patterns read as uint64; int64 tensors are accepted as raw storage)."""
     _dev_tensor(keys, (8,))
     st = Stats() if stats else None
     rc = lib().dfr_sort_u64_ex(keys.data_ptr(), keys.numel(), _stream(stream),
                                ctypes.byref(_cfg(n_d, skip_trivial, events, fused,
-                                                 fast_radix=fast_radix)),
+                                                 fast_radix=fast_radix,
+                                                 stable_deals=stable_deals)),
                                ctypes.byref(st) if st is not None else None)
     _check(rc, "dfr_sort_u64")
     return st.as_dict() if st is not None else None

@@ -475,14 +475,16 @@ static Params<K> make_params(char* ws, const Layout& L, K* keys, uint32_t* vals,
 }
 
 static int cfg_nd(const dfr_config* cfg, uint32_t* n_d, uint32_t* skip, uint32_t* nofuse,
-                  uint32_t* full_lsd, uint32_t* fast_radix) {
+                  uint32_t* full_lsd, uint32_t* fast_radix, uint32_t* stable) {
+  *stable = 0;
   *n_d = DFR_DEFAULT_ND;
   *skip = 1;
   *nofuse = 0;
   *full_lsd = 0;
   *fast_radix = 0;
   if (cfg) {
-    if (cfg->fast_radix > 1) return DFR_ERR_INVALID;
+    if (cfg->fast_radix > 1 || cfg->stable_deals > 1) return DFR_ERR_INVALID;
+    *stable = cfg->stable_deals;
     *fast_radix = cfg->fast_radix;
     if (cfg->full_lsd > 1) return DFR_ERR_INVALID;
     *full_lsd = cfg->full_lsd;
@@ -499,8 +501,9 @@ template <class K, bool PAIRS>
 static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const dfr_config* cfg,
                      dfr_stats* stats) {
   using Ph = Phases<K, PAIRS>;
-  uint32_t n_d, skip, nofuse, full_lsd, fast_radix;
-  if (cfg_nd(cfg, &n_d, &skip, &nofuse, &full_lsd, &fast_radix) != DFR_OK) return DFR_ERR_INVALID;
+  uint32_t n_d, skip, nofuse, full_lsd, fast_radix, stable;
+  if (cfg_nd(cfg, &n_d, &skip, &nofuse, &full_lsd, &fast_radix, &stable) != DFR_OK)
+    return DFR_ERR_INVALID;
   if (full_lsd && sizeof(K) > (size_t)MAX_PASSES) return DFR_ERR_INVALID;  // D = 8 > passes a group holds
   if (stats) memset(stats, 0, sizeof(*stats));
   if (n <= 1) return DFR_OK;
@@ -533,6 +536,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
   Params<K> P = make_params<K>(ws, L, keys, vals, PAIRS, n_d, skip, n);
   P.fuse = fuse ? 1u : 0u;
   P.full_lsd = full_lsd;
+  P.unstable = (!PAIRS && !stable) ? 1u : 0u;
   const uint32_t nn = (uint32_t)n;
   const int sms = dv.sms;
   const PhaseEv pe{cfg ? cfg->phase_events : nullptr, st};

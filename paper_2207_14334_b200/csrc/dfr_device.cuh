@@ -171,6 +171,12 @@ struct Params {
   uint32_t* J;          // fused level 0: [256][16] counts of (top digit, top 4 bits of the
                         // middle digit), then [16][256] chain bases (exclusive over chains)
   uint32_t skip_trivial;
+  // keys only (dfr_config.stable_deals == 0): a deal whose tile is constant in
+  // the group digits below its own ranks keys of equal digit in any order
+  // (shared-memory atomics instead of the ballot multi-split).  Output-
+  // invariant: equal keys are indistinguishable, every later pass of the group
+  // is stable, and the buckets are then sorted on all lower digits (DESIGN R5)
+  uint32_t unstable;
   uint32_t full_lsd;    // ablation: the top call sorts all D digits LSD (dfr_config.full_lsd)
   // Fast Radix estimation (dfr_config.fast_radix; Alg. 3): the
   // level-0 pass on the lowest group digit deals into ESTIMATED buckets of
@@ -317,6 +323,12 @@ __device__ __forceinline__ __half2 __ushort_as_half2_pair(uint32_t h) {
 __device__ __forceinline__ __half2 u2h2(uint32_t v) { return *reinterpret_cast<const __half2*>(&v); }
 __device__ __forceinline__ void red_add_shared(uint32_t saddr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+// shared-memory add returning the old value (ATOMS.ADD)
+__device__ __forceinline__ uint32_t atom_add_shared(uint32_t saddr, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(saddr), "r"(v) : "memory");
+  return r;
 }
 
 // least p >= 0 with len <= n_d * 256^p  (Alg. 4 l.4; reading S:284)

@@ -527,7 +527,7 @@ struct Phases {
                                                    uint32_t* status, K* sk, V* sv, uint32_t* whist,
                                                    int* s_dst, uint32_t* s_warp, K* dst, V* dstv,
                                                    uint32_t bstart, uint16_t* perm, uint32_t sup,
-                                                   uint32_t nh_s = 0) {
+                                                   uint32_t nh_s, bool uns) {
     constexpr int SC_W = SC_NT / 32;
     constexpr int SC_KPT = TILE / SC_NT;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -538,15 +538,29 @@ struct Phases {
     V val[SC_KPT];
     uint32_t dr[SC_KPT];
     const uint32_t tc_s = smem_u32(tcount);
+    uns = !PAIRS && uns;
+    if (uns) {  // (R5) rank = the tile counter's old value: keys of equal digit in any order
 #pragma unroll
-    for (int jj = 0; jj < SC_KPT; ++jj) {
-      const uint32_t idx = w * 32 * SC_KPT + jj * 32 + lane;
-      key[jj] = sk[(PERM ? (sup & 0xffu) : 0u) + idx];  // PERM: the tile starts koff into sk
-      if (PAIRS && !PERM) val[jj] = sv[idx];
-      dr[jj] = (FULL || idx < cnt) ? digit_of(key[jj], dg) : 256u;
-      if (FULL || idx < cnt) {
-        red_add_shared(tc_s + 4 * dr[jj], 1u);  // tile histogram
-        if (FRM) red_add_shared(nh_s + 4 * digit_of(key[jj], dg + 1), 1u);  // the next digit (Alg. 3 l.5-6)
+      for (int jj = 0; jj < SC_KPT; ++jj) {
+        const uint32_t idx = w * 32 * SC_KPT + jj * 32 + lane;
+        key[jj] = sk[(PERM ? (sup & 0xffu) : 0u) + idx];
+        dr[jj] = (FULL || idx < cnt) ? digit_of(key[jj], dg) : 256u;
+        if (FULL || idx < cnt) {
+          dr[jj] |= atom_add_shared(tc_s + 4 * dr[jj], 1u) << 16;
+          if (FRM) red_add_shared(nh_s + 4 * digit_of(key[jj], dg + 1), 1u);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < SC_KPT; ++jj) {
+        const uint32_t idx = w * 32 * SC_KPT + jj * 32 + lane;
+        key[jj] = sk[(PERM ? (sup & 0xffu) : 0u) + idx];  // PERM: the tile starts koff into sk
+        if (PAIRS && !PERM) val[jj] = sv[idx];
+        dr[jj] = (FULL || idx < cnt) ? digit_of(key[jj], dg) : 256u;
+        if (FULL || idx < cnt) {
+          red_add_shared(tc_s + 4 * dr[jj], 1u);  // tile histogram
+          if (FRM) red_add_shared(nh_s + 4 * digit_of(key[jj], dg + 1), 1u);  // the next digit (Alg. 3 l.5-6)
+        }
       }
     }
     __syncthreads();
@@ -594,29 +608,36 @@ struct Phases {
       }
       *reinterpret_cast<uint4*>(s_dst + 8 * lane) = make_uint4(ex[0], ex[1], ex[2], ex[3]);
       *reinterpret_cast<uint4*>(s_dst + 8 * lane + 4) = make_uint4(ex[4], ex[5], ex[6], ex[7]);
+      if (uns) {  // the reorder's bases (s_dst is rewritten by the look-back meanwhile)
+        *reinterpret_cast<uint4*>(whist + 8 * lane) = make_uint4(ex[0], ex[1], ex[2], ex[3]);
+        *reinterpret_cast<uint4*>(whist + 8 * lane + 4) = make_uint4(ex[4], ex[5], ex[6], ex[7]);
+      }
     }
-    warp_rank<SC_KPT, FULL, PERM>(dr, mywh);
+    if (!uns) warp_rank<SC_KPT, FULL, PERM>(dr, mywh);
     __syncthreads();  // ranks and tile offsets done
     // per digit: warp bases in the tile = tile offset of the digit + counts of
     // the digit in earlier warps
     uint32_t lstart = 0;
-    if (dig_thread) {
-      lstart = (uint32_t)s_dst[dd];
-      uint32_t acc = lstart;
+    if (dig_thread) lstart = (uint32_t)s_dst[dd];
+    if (!uns) {
+      if (dig_thread) {
+        uint32_t acc = lstart;
 #pragma unroll
-      for (int e = 0; e < SC_W; ++e) {
-        const uint32_t x = whist[e * 256 + dd];
-        whist[e * 256 + dd] = acc;
-        acc += x;
+        for (int e = 0; e < SC_W; ++e) {
+          const uint32_t x = whist[e * 256 + dd];
+          whist[e * 256 + dd] = acc;
+          acc += x;
+        }
       }
+      __syncthreads();
     }
-    __syncthreads();
-    // reorder the tile by digit in shared memory (stable)
+    // reorder the tile by digit in shared memory (stable unless uns)
+    const uint32_t* const rb = uns ? whist : mywh;
 #pragma unroll
     for (int jj = 0; jj < SC_KPT; ++jj) {
       const uint32_t dgt = dr[jj] & 0xffffu;
       if (FULL || dgt < 256) {
-        const uint32_t pos = mywh[dgt] + (dr[jj] >> 16);
+        const uint32_t pos = rb[dgt] + (dr[jj] >> 16);
         if (PERM) {
           perm[pos] = (uint16_t)((sup & 0xffu) + w * 32 * SC_KPT + jj * 32 + lane);
         } else {
@@ -914,14 +935,26 @@ struct Phases {
           for (uint32_t i = threadIdx.x; i < cnt; i += SC_NT) sv[i] = srcv[base + i];
         __syncthreads();
       }
+      // (R5) keys only: ranks in any order when the tile is constant in the
+      // group digits below dg (the input of pass j is sorted by them)
+      bool uns = false;
+      if (!PAIRS && P.unstable) {
+        if (j == 0) {
+          uns = true;
+        } else {
+          const K* tk = sk + (PERM ? (sup & 0xffu) : 0u);
+          const K x = (tk[0] ^ tk[cnt - 1]) >> (8 * s.low);
+          uns = (x & ((K(1) << (8 * j)) - 1)) == 0;
+        }
+      }
       if (cnt == (uint32_t)TILE)
         deal_tile<SC_NT, true, FUSEH, PERM, FRM>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist,
                                                  s_dst, s_warp, dst, dstv, bstart, perm, sup,
-                                                 smem_u32(nh));
+                                                 smem_u32(nh), uns);
       else
         deal_tile<SC_NT, false, FUSEH, PERM, FRM>(hook, P, s, j, t, lt, cnt, dg, status, sk, sv, whist,
                                                   s_dst, s_warp, dst, dstv, bstart, perm, sup,
-                                                  smem_u32(nh));
+                                                  smem_u32(nh), uns);
       if (PERM) {  // single buffer: refill it once every thread is done with the write-out
         for (int e = threadIdx.x; e < (SC_W + 1) * 256; e += SC_NT) whist[e] = 0;
         __syncthreads();

@@ -53,6 +53,8 @@ def test_trivial_calls_need_no_device():
     assert L.dfr_sort_u64_ex(None, 10, None, ctypes.byref(bad), None) == dfr.DFR_ERR_INVALID
     bad = dfr.Config(64, 1, None, 3)  # fused_last_pass out of range
     assert L.dfr_sort_u64_ex(None, 10, None, ctypes.byref(bad), None) == dfr.DFR_ERR_INVALID
+    bad = dfr.Config(64, 1, None, 0, 0, 0, 2)  # stable_deals out of range
+    assert L.dfr_sort_u64_ex(None, 10, None, ctypes.byref(bad), None) == dfr.DFR_ERR_INVALID
     lsd = dfr.Config(64, 1, None, 0, 1)  # the full-LSD ablation holds 4 digits: not u64
     assert L.dfr_sort_u64_ex(ctypes.c_void_p(0x1000), 10, None, ctypes.byref(lsd), None) == dfr.DFR_ERR_INVALID
     # null pointer with n > 1
