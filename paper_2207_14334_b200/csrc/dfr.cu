@@ -346,10 +346,10 @@ static cudaError_t get_dev(Dev& out) {
     setup((const void*)k_mid_s<K, PAIRS>, Ph::SMEM_MID_S, &d.occ_mid_s);
     if (err == cudaSuccess) {  // fused last pass: FNT-thread CTAs
       err = cudaFuncSetAttribute((const void*)k_fused<K, PAIRS>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_FUSED);
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_FUSED_X);
       if (err == cudaSuccess)
         err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_fused, (const void*)k_fused<K, PAIRS>,
-                                                            Ph::FNT, Ph::SMEM_FUSED);
+                                                            Ph::FNT, Ph::SMEM_FUSED_X);
     }
     setup((const void*)k_levels<K, PAIRS>, Ph::SMEM_LEVEL, &d.occ_levels);
     if (err == cudaSuccess && !PAIRS) {  // keys-only mid rounds: FNT-thread CTAs
@@ -605,7 +605,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
       if (fuse && j == 2) {  // run-aligned tiles, then the fused last deal + diversion
         launch_pdl(k_fplan<K, PAIRS>, 1, 1024, 0, st, P);
         const int g_f = sms * std::max(1, dv.occ_fused);
-        launch_pdl(k_fused<K, PAIRS>, g_f, Ph::FNT, Ph::SMEM_FUSED, st, P);
+        launch_pdl(k_fused<K, PAIRS>, g_f, Ph::FNT, Ph::SMEM_FUSED_X, st, P);
         g_launches += 2;
       }
       if (fuse && j == 1 && !PAIRS)

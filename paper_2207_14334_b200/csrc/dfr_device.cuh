@@ -49,6 +49,18 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_HIST_TILES
 #define DFR_HIST_TILES 8  // histogram: deal tiles counted per step of its tile loop
 #endif
+#ifndef DFR_DEAL_PF
+#define DFR_DEAL_PF 1  // deal: L2 prefetch of the next tile when its ticket is claimed
+#endif
+#ifndef DFR_FUSED_SB
+#define DFR_FUSED_SB 3  // fused pass: sub-bucket bits below the group (4 or 8 sub-buckets per digit)
+#endif
+#ifndef DFR_LB_EARLY
+#define DFR_LB_EARLY 0  // deal: the look-back's first round trip issued before the reorder
+#endif
+#ifndef DFR_HIST_COPIES
+#define DFR_HIST_COPIES 1  // histogram: shared-memory counter sets per CTA (warp w uses w % copies)
+#endif
 #ifndef DFR_HIST_U
 #define DFR_HIST_U 8  // histogram: 16-byte loads in flight per thread
 #endif
@@ -62,11 +74,13 @@ constexpr int WARPS = THREADS / 32;
 #define DFR_DV_CU 1  // diversion rank-count loop unroll
 #endif
 #ifndef DFR_FLB
-#define DFR_FLB 8  // fused pass: look-back predecessors loaded per round trip
+#define DFR_FLB 4  // fused pass: look-back predecessors loaded per round trip
 #endif
 constexpr int LB_PAD = 32;  // status rows in front of pass 0's table (>= DFR_LB, DFR_FLB)
 static_assert(DFR_LB <= LB_PAD && DFR_FLB <= LB_PAD, "look-back pad");
 constexpr int WO_UNROLL = DFR_WO_UNROLL, DV_CU = DFR_DV_CU;
+constexpr int HCOPIES = DFR_HIST_COPIES;
+static_assert(WARPS % HCOPIES == 0, "histogram copies");
 constexpr int KPT = 16;                  // keys per thread per tile
 constexpr int TILE = THREADS * KPT;      // 4096 keys per tile (hist / deal)
 #ifndef DFR_WIN

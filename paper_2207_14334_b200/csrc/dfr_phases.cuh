@@ -67,7 +67,7 @@ struct Phases {
 
   // ------------------------------------------------------------ smem sizes
   // warp-private digit counters + the fused level's chain histogram (256 x 16)
-  static constexpr size_t SMEM_HIST = WARPS * MAX_PASSES * 256 * 4 + 4096 * 4 + 64;
+  static constexpr size_t SMEM_HIST = HCOPIES * MAX_PASSES * 256 * 4 + 4096 * 4 + 64;
   static constexpr int F_CHAINS = 16;  // fused pass: chains = top 4 bits of the middle digit
   // The deal kernel runs SC_NT threads per CTA over tiles of TILE keys
   // (4 CTAs/SM with the permutation deal: 32 warps hide the look-back and load latencies)
@@ -200,7 +200,7 @@ struct Phases {
     for (uint32_t j = 0; j < s.p; ++j) {
       uint32_t v = 0;
 #pragma unroll
-      for (int w = 0; w < WARPS; ++w) {
+      for (int w = 0; w < HCOPIES; ++w) {
         v += sh[(w * MAX_PASSES + j) * 256 + threadIdx.x];
         sh[(w * MAX_PASSES + j) * 256 + threadIdx.x] = 0;
       }
@@ -352,11 +352,11 @@ struct Phases {
     const uint32_t t0 = blockIdx.x * per;
     const uint32_t t1 = min(total, t0 + per);
     if (t0 >= t1) return;
-    uint32_t* sh = sm;  // [WARPS][MAX_PASSES][256]
-    const uint32_t shw = smem_u32(sh + (threadIdx.x >> 5) * MAX_PASSES * 256);
-    for (int j = 0; j < WARPS * MAX_PASSES; ++j) sh[j * 256 + threadIdx.x] = 0;
+    uint32_t* sh = sm;  // [HCOPIES][MAX_PASSES][256]; warp w counts into copy w % HCOPIES
+    const uint32_t shw = smem_u32(sh + ((threadIdx.x >> 5) % HCOPIES) * MAX_PASSES * 256);
+    for (int j = 0; j < HCOPIES * MAX_PASSES; ++j) sh[j * 256 + threadIdx.x] = 0;
     // the fused level: also the (top digit, chain) histogram of the group
-    uint32_t* jh = (P.fuse && c->level == 0) ? sm + WARPS * MAX_PASSES * 256 : nullptr;
+    uint32_t* jh = (P.fuse && c->level == 0) ? sm + HCOPIES * MAX_PASSES * 256 : nullptr;
     const uint32_t jsh = jh ? smem_u32(jh) : 0u;
     if (jh)
       for (uint32_t x = threadIdx.x; x < 4096u; x += THREADS) jh[x] = 0;
@@ -582,9 +582,15 @@ struct Phases {
     const uint32_t dd = threadIdx.x;
     const bool dig_thread = dd < 256;
     uint32_t run = 0;
+    constexpr int LB = DFR_LB;  // predecessors per look-back round trip
+    uint32_t lbv[LB];
     if (dig_thread) {
       run = tcount[dd];
       st_relaxed(status + (size_t)t * 256 + dd, (lt == 0 ? FLAG_INC : FLAG_AGG) | run);
+#if DFR_LB_EARLY
+      // the look-back's first round trip, in flight during the reorder
+      if (lt > 0) ld_lookback<LB>(status + (size_t)(t - 1) * 256 + dd, lbv);
+#endif
     }
     if (w == 0) {  // tile offsets of the 256 digits (8 per lane) into s_dst, free until the look-back
       const uint4 c0 = *reinterpret_cast<const uint4*>(tcount + 8 * lane);
@@ -654,14 +660,20 @@ struct Phases {
       if (lt > 0) {  // decoupled look-back, up to LB predecessors per round trip
 #endif
         int tt = (int)t - 1;
+        bool first = true;
         while (true) {
-          constexpr int LB = DFR_LB;  // predecessors per look-back round trip
           // LB predecessors tt, tt-1, ... in one round trip; rows before the
           // segment's first tile t0 may be read (status has LB pad rows in
           // front) but are never used: t0 publishes FLAG_INC, and the walk
           // stops at the first FLAG_INC or unpublished entry
           uint32_t v[LB];
-          ld_lookback<LB>(status + (size_t)tt * 256 + dd, v);
+          if (DFR_LB_EARLY && first) {
+#pragma unroll
+            for (int i = 0; i < LB; ++i) v[i] = lbv[i];
+          } else {
+            ld_lookback<LB>(status + (size_t)tt * 256 + dd, v);
+          }
+          first = false;
           int k = 0;
           bool done = false;
 #pragma unroll
@@ -784,6 +796,19 @@ struct Phases {
       return;
     }
     ti[2] = 1;
+#if DFR_DEAL_PF
+    // the copy starts only after the current tile's write-out: pull the
+    // tile into L2 meanwhile
+    if (DEFER) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(TILE * sizeof(K)))
+                   : "memory");
+      if (PAIRS) {
+        const uintptr_t b = reinterpret_cast<uintptr_t>(srcv) & ~(uintptr_t)15;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b), "r"((uint32_t)(TILE * 4)) : "memory");
+      }
+    }
+#endif
     if (!DEFER) issue_tile<SUP, FRM>(P, j, q, ti, kb, vb, bar);
   }
   static __device__ __forceinline__ uint32_t sup_bytes(uintptr_t head, uint32_t bytes) {
@@ -1884,8 +1909,101 @@ struct Phases {
     }
   }
 
+  // ---- the fused pass with exact composites.  Inside a tile (one s-run) the
+  // keys are split by (hi, the top GSB remaining bits) into sub-buckets, which
+  // are already in order; inside a sub-bucket every key's remaining bits sit
+  // at the top of a composite c = (k << G_CSH) | sb << 13 | slot (the slot, the
+  // key's arrival rank in its sub-bucket, breaks ties between equal keys), so
+  // the composites of a sub-bucket are distinct and ordered exactly as the
+  // (key, slot) pairs: a key's rank is the number of sub-bucket composites
+  // below its own -- no lossy compare, no tie fix-up.  The composite also
+  // carries everything the write-out needs to rebuild the key (sb gives hi and
+  // the sub-bucket bits; the tile's (mid, lo) bits are common), so one array
+  // holds the tile: composites at their slot positions while ranking, then at
+  // their final positions for the write-out.
+  static constexpr int GSB = DFR_FUSED_SB;                  // sub-bucket bits below the group
+  static constexpr int GNS = 256 << GSB;                    // sub-buckets per tile
+  static constexpr int G_SBS = 8 * F_LOW - GSB;             // lowest sub-bucket bit
+  static constexpr int G_CSH = 8 * (int)sizeof(K) - G_SBS;  // remaining bits -> top of c
+  static_assert(G_CSH >= 13 + 8 + GSB, "composite fields: slot (13 bits) and sub-bucket");
+  static_assert(GNS / 256 == 8 || GNS / 256 == 4, "4 or 8 sub-buckets per digit value");
+  struct FX {                                              // shared-memory layout, byte offsets
+    static constexpr int KEYS = 0;                         // K[FT_MAX + 4] composites (4 pad: rank loads)
+    static constexpr int POS = KEYS + (FT_MAX + 4) * (int)sizeof(K);  // u16[FT_MAX]: final tile position
+    static constexpr int CNT = POS + FT_MAX * 2;           // u32[2][GNS] (two tiles)
+    static constexpr int BDESC = CNT + 2 * GNS * 4;        // u32[GNS]: start | compare count << 13
+    static constexpr int SDST = BDESC + GNS * 4;           // int[256]
+    static constexpr int WARP = SDST + 1024;               // u32[16]
+    static constexpr int MISC = WARP + 64;                 // u32[16]: tickets; [8..11] the two tiles' prefixes
+    static constexpr int BYTES = MISC + 64;
+  };
+  static_assert(FX::CNT % 16 == 0 && FX::BDESC % 16 == 0 && FX::MISC % 16 == 0, "fused smem alignment");
+  static constexpr size_t SMEM_FUSED_X = FX::BYTES;
+  static constexpr K G_PRE = (K(1) << (8 * F_DG)) - (K(1) << (8 * F_LOW));  // the (mid, lo) bits
+  static __device__ __forceinline__ uint32_t g_sub(K k) {
+    return (uint32_t)(k >> (8 * F_DG)) << GSB | ((uint32_t)(k >> G_SBS) & ((1u << GSB) - 1));
+  }
+  // u64: the composite is the key rotated left by G_CSH: the remaining bits
+  // on top, the (hi, mid, lo, sub-bucket) bits -- constant in a sub-bucket --
+  // below; equal keys tie (checked).  u32: the 5 remaining bits on top, then
+  // the sub-bucket and the slot: unique, exact.
+  static constexpr bool LOSSY = sizeof(K) == 8;
+  static __device__ __forceinline__ K g_comp(K k, uint32_t sb, uint32_t slot) {
+    if constexpr (LOSSY)
+      return k << G_CSH | k >> (8 * sizeof(K) - G_CSH);
+    else
+      return k << G_CSH | (K)(sb << 13 | slot);
+  }
+  static __device__ __forceinline__ uint32_t g_hi(K cpt) {  // the top digit of the key
+    if constexpr (LOSSY)
+      return (uint32_t)(cpt >> (8 * F_DG - G_SBS)) & 255u;
+    else
+      return (uint32_t)(cpt >> (13 + GSB)) & 255u;
+  }
+  static __device__ __forceinline__ K g_key(K cpt, K pre) {
+    if constexpr (LOSSY) {
+      return cpt >> G_CSH | cpt << (8 * sizeof(K) - G_CSH);
+    } else {
+      const uint32_t sb = (uint32_t)(cpt >> 13) & (GNS - 1);
+      return (K)(sb >> GSB) << (8 * F_DG) | pre | (K)(sb & ((1u << GSB) - 1)) << G_SBS | cpt >> G_CSH;
+    }
+  }
+  // composites in shared memory as two word arrays (u64: top words, then
+  // low words; u32: one array), so that the rank loads of top words spread
+  // over all 32 banks
+  static constexpr int G_WORDS = FT_MAX + 4;  // 4 pad entries: the rank's 4-wide loads
+  static __device__ __forceinline__ void st_comp(uint32_t a, uint32_t x, K c) {
+    sts32(a + 4 * x, (uint32_t)(c >> (8 * sizeof(K) - 32)));
+    if constexpr (sizeof(K) == 8) sts32(a + 4 * (G_WORDS + x), (uint32_t)c);
+  }
+  static __device__ __forceinline__ K ld_comp(uint32_t a, uint32_t x) {
+    if constexpr (sizeof(K) == 8)
+      return (K)lds32(a + 4 * x) << 32 | lds32(a + 4 * (G_WORDS + x));
+    else
+      return (K)lds32(a + 4 * x);
+  }
+  // exact ranks of every key of the tile in a small sub-bucket: full
+  // composites, the slot breaking ties (the tile had tied top words)
+  // (inlined: the register arrays must not be passed by address)
+  static __device__ __forceinline__ void fused_exact(const K (&key)[FKPT], const uint32_t (&ds)[FKPT],
+                                                     uint32_t keys_a, uint32_t pos_a) {
+#pragma unroll
+    for (int m = 0; m < FKPT; ++m) {
+      if (ds[m] == ~0u) continue;
+      const uint32_t cb = (ds[m] >> 13) & 511u;
+      if (!cb) continue;
+      const uint32_t x = ds[m] & 8191u, slot = ds[m] >> 22, bl = x - slot;
+      uint32_t r = 0;
+      for (uint32_t z = 0; z < cb; ++z) {
+        const K cz = ld_comp(keys_a, bl + z);
+        r += cz < key[m] || (cz == key[m] && z < slot);
+      }
+      sts16(pos_a + 2 * x, bl + r);
+    }
+  }
+
   static __device__ void fused(const Params<K>& P, uint32_t* sm) {
-    constexpr bool LOSSY = sizeof(K) == 8;
+    constexpr int SBW = 8 + GSB;  // ds: sub-bucket | slot << SBW
     Ctl* c = P.ctl;
     if (!*(volatile uint32_t*)&c->fused_ok) return;
     const Seg sv = P.segq[c->cur][0];
@@ -1894,25 +2012,23 @@ struct Phases {
     const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t nd = P.n_d;
     char* base = reinterpret_cast<char*>(sm);
-    uint32_t* bdesc = reinterpret_cast<uint32_t*>(base + FS::BDESC);
-    int* s_dst = reinterpret_cast<int*>(base + FS::SDST);
-    uint32_t* flag = reinterpret_cast<uint32_t*>(base + FS::FLAG);
-    uint32_t* s_warp = reinterpret_cast<uint32_t*>(base + FS::WARP);
-    uint32_t* misc = reinterpret_cast<uint32_t*>(base + FS::MISC);
-    const uint32_t keys_a = smem_u32(base + FS::KEYS), cmp_a = smem_u32(base + FS::CMP),
-                   cnt0_a = smem_u32(base + FS::CNT),
-                   pos_a = smem_u32(base + FS::POS);
+    uint32_t* bdesc = reinterpret_cast<uint32_t*>(base + FX::BDESC);
+    int* s_dst = reinterpret_cast<int*>(base + FX::SDST);
+    uint32_t* s_warp = reinterpret_cast<uint32_t*>(base + FX::WARP);
+    uint32_t* misc = reinterpret_cast<uint32_t*>(base + FX::MISC);
+    const uint32_t keys_a = smem_u32(base + FX::KEYS), cnt0_a = smem_u32(base + FX::CNT),
+                   pos_a = smem_u32(base + FX::POS);
     uint32_t* status = P.status + (size_t)j * P.status_stride;
     const K* src = P.kbuf(route_src(sv, j)) + sv.start;
     K* const out = P.A;
-    const uint32_t d = threadIdx.x;  // phase 2, look-back: one thread per digit value
+    const uint32_t d = threadIdx.x;  // layout, look-back: one thread per digit value
     const uint32_t brow = P.hist[(size_t)(sv.hist_off + j) * 256 + d];  // bucket offsets of the top digit
     const uint32_t kofs = w * 32 * FKPT + lane;  // this thread's first key of a tile
-    auto cnt_of = [&](uint32_t cb) { return reinterpret_cast<uint32_t*>(base + FS::CNT + cb * FNS * 4); };
+    auto cnt_of = [&](uint32_t cb) { return reinterpret_cast<uint32_t*>(base + FX::CNT + cb * GNS * 4); };
     K key[FKPT];
-    uint32_t ds[FKPT];  // sub-bucket | slot << 10, or ~0u
-    // keys of tile tt -> registers; sub-bucket and slot of every key (counter set cb)
-    // ... and the tile's chain link (ticket of its predecessor in the chain, or ~0u) and chain
+    uint32_t ds[FKPT];  // sub-bucket | slot << SBW; then slot position | compare count << 13 | slot << 22;
+                        // then final position; ~0u: no key
+    // keys of tile tt -> registers, with the tile's chain link and chain
     auto load_keys = [&](uint32_t tt, uint32_t& prev, uint32_t& chn) -> uint32_t {
       uint32_t ln = 0;
       if (tt < ntiles) {
@@ -1927,20 +2043,29 @@ struct Phases {
       }
       return ln;
     };
+    // sub-bucket and slot of every key (counter set cb); the tile's (mid, lo) bits
     auto count_keys = [&](uint32_t ln, uint32_t cb) {
-      {
-        const int lim = (int)ln - (int)kofs;
-        const uint32_t ca = cnt0_a + cb * FNS * 4;
+      const int lim = (int)ln - (int)kofs;
+      const uint32_t ca = cnt0_a + cb * GNS * 4;
 #pragma unroll
-        for (int m = 0; m < FKPT; ++m) {
-          ds[m] = ~0u;
-          if (m * 32 < lim) {
-            const uint32_t sb = f_sub(key[m]);
-            uint32_t slot;
-            asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(slot) : "r"(ca + 4 * sb) : "memory");
-            ds[m] = sb | slot << 10;
-          }
+      for (int m = 0; m < FKPT; ++m) {
+        ds[m] = ~0u;
+        if (m * 32 < lim) {
+          const uint32_t sb = g_sub(key[m]);
+          ds[m] = sb | atom_add_shared(ca + 4 * sb, 1u) << SBW;
         }
+      }
+      if (threadIdx.x == 0 && ln) *reinterpret_cast<K*>(misc + 8 + 2 * cb) = key[0] & G_PRE;
+    };
+    auto digit_counts = [&](uint32_t cb, uint32_t (&cs)[GNS / 256]) {
+      const uint4* p = reinterpret_cast<const uint4*>(cnt_of(cb)) + (GNS / 1024) * d;
+#pragma unroll
+      for (int r = 0; r < GNS / 1024; ++r) {
+        const uint4 v = p[r];
+        cs[4 * r] = v.x;
+        cs[4 * r + 1] = v.y;
+        cs[4 * r + 2] = v.z;
+        cs[4 * r + 3] = v.w;
       }
     };
     // the tile aggregate of digit d, published as soon as the counts are
@@ -1950,21 +2075,27 @@ struct Phases {
     const uint32_t regular = c->fused_regular, chains = c->fused_chains;
     auto publish = [&](uint32_t tt, uint32_t cb, uint32_t prev, uint32_t chn) {
       if (tt < ntiles) {
-        const uint4 c4 = reinterpret_cast<const uint4*>(cnt_of(cb))[d];
-        const uint32_t cdd = c4.x + c4.y + c4.z + c4.w;
+        uint32_t cs[GNS / 256];
+        digit_counts(cb, cs);
+        uint32_t cdd = 0;
+#pragma unroll
+        for (int r = 0; r < GNS / 256; ++r) cdd += cs[r];
         st_relaxed(status + (size_t)tt * 256 + d,
                    prev == ~0u ? (FLAG_INC | (jbase[chn * 256 + d] + cdd)) : (FLAG_AGG | cdd));
       }
     };
-    reinterpret_cast<uint4*>(cnt_of(0))[d] = make_uint4(0, 0, 0, 0);
-    reinterpret_cast<uint4*>(cnt_of(1))[d] = make_uint4(0, 0, 0, 0);
-    if (d < FNS / 32) flag[d] = 0;
+    auto zero_counts = [&](uint32_t cb) {
+      uint4* p = reinterpret_cast<uint4*>(cnt_of(cb)) + (GNS / 1024) * d;
+#pragma unroll
+      for (int r = 0; r < GNS / 1024; ++r) p[r] = make_uint4(0, 0, 0, 0);
+    };
+    zero_counts(0);
+    zero_counts(1);
     // tickets are claimed one tile ahead, so that a tile's keys are in L2
     // (bulk prefetch at its claim) by the time they are loaded
     if (d == 0) {
       misc[0] = atomicAdd(&c->fticket, 1u);
       misc[1] = atomicAdd(&c->fticket, 1u);
-      misc[3] = 0;
       if (misc[1] < ntiles) {
         const uint4 tn = P.ftiles[misc[1]];
         prefetch_keys_l2(src + tn.x, tn.y);
@@ -1982,100 +2113,93 @@ struct Phases {
     publish(t, 0, tprev, tch);
     while (t < ntiles) {
       FPROF_MARK(0);  // (the previous tile's tail)
-      // ---- 2: bucket layout (thread d: digit value d and its sub-buckets)
-      static_assert(FSB == 2, "four sub-buckets per digit value");
-      const uint4 c4 = reinterpret_cast<const uint4*>(cnt_of(cur))[d];
-      const uint32_t cs[4] = {c4.x, c4.y, c4.z, c4.w};
-      const uint32_t cd = c4.x + c4.y + c4.z + c4.w;
+      // ---- layout (thread d: digit value d and its sub-buckets)
+      uint32_t cs[GNS / 256];
+      digit_counts(cur, cs);
+      uint32_t cd = 0;
+#pragma unroll
+      for (int r = 0; r < GNS / 256; ++r) cd += cs[r];
       const bool small = cd <= nd;
-      uint32_t padc = 0;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) padc += (small && cs[r] >= 2) ? (cs[r] + 3) & ~3u : 0u;
-      const uint32_t ex = fused_scan(cd | padc << 16, s_warp);
-      const uint32_t lst = ex & 0xffffu;
+      if (d == 0) misc[3] = 0;  // the tile's tie check (the last tile's was read before this barrier)
+      const uint32_t lst = fused_scan(cd, s_warp);  // the bucket's first tile position
       {
-        uint32_t so = lst, co = ex >> 16;
-        uint32_t bd[4];
+        uint32_t so = lst, bd[GNS / 256];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const uint32_t ng = (small && cs[r] >= 2) ? (cs[r] + 3) >> 2 : 0u;
-          bd[r] = (co >> 2) | ng << 11 | so << 18;
-          // the last group of the area := +inf; phase 3 overwrites its real entries
-          if (ng) sts64(cmp_a + 2 * (co + 4 * ng - 4), 0x7c007c007c007c00ull);
+        for (int r = 0; r < GNS / 256; ++r) {
+          bd[r] = so | ((small && cs[r] >= 2) ? cs[r] : 0u) << 13;
           so += cs[r];
-          co += 4 * ng;
         }
-        reinterpret_cast<uint4*>(bdesc)[d] = make_uint4(bd[0], bd[1], bd[2], bd[3]);
+        uint4* bp = reinterpret_cast<uint4*>(bdesc) + (GNS / 1024) * d;
+#pragma unroll
+        for (int r = 0; r < GNS / 1024; ++r) bp[r] = make_uint4(bd[4 * r], bd[4 * r + 1], bd[4 * r + 2], bd[4 * r + 3]);
       }
       __syncthreads();
       FPROF_MARK(1);
-      // ---- 3: keys grouped by sub-bucket, composites of small-bucket keys
-      if (d == 0) misc[3] = 0;  // the tile's tie check accumulator (read before phase 2's barrier)
+      // the ticket after the next one (consumed after the ranks: the atomic is
+      // in flight meanwhile)
+      uint32_t tw = 0;
+      if (d == 0) tw = atomicAdd(&c->fticket, 1u);
+      // ---- composites at their slot positions
 #pragma unroll
       for (int m = 0; m < FKPT; ++m) {
         if (ds[m] != ~0u) {
-          const uint32_t slot = ds[m] >> 10;
-          const uint32_t bd = bdesc[ds[m] & (FNS - 1)];
-          const uint32_t x = (bd >> 18) + slot;
-          if constexpr (sizeof(K) == 8)
-            sts64(keys_a + 8 * x, (unsigned long long)key[m]);
-          else
-            sts32(keys_a + 4 * x, (uint32_t)key[m]);
-          if ((bd >> 11) & 127u) sts16(cmp_a + 2 * (4 * (bd & 2047u) + slot), f_comp(key[m], slot));
+          const uint32_t sb = ds[m] & (GNS - 1), slot = ds[m] >> SBW;
+          const uint32_t bd = bdesc[sb];
+          const uint32_t x = (bd & 8191u) + slot, cb = bd >> 13;
+          key[m] = g_comp(key[m], sb, slot);
+          st_comp(keys_a, x, key[m]);
+          ds[m] = x | cb << 13 | (cb ? slot << 22 : 0u);
         }
       }
       __syncthreads();
       FPROF_MARK(2);
-      // ---- 4: slot-major rank inside each sub-bucket -> final tile position.
-      // Without ties the positions are a permutation of the slots, so the
-      // sum over the tile of (position - slot) is 0; tied keys share the lower
-      // rank, which makes it negative (checked after the write-out)
+      // ---- ranks: the number of smaller composites in the sub-bucket.  u64:
+      // the top words of equal keys (or, with odds 2^-32 per pair, of keys
+      // that differ only in their low bits) tie and share the lower rank; the
+      // sum over the tile of (rank - slot) is then negative, and the tile is
+      // re-ranked exactly on the full composites (slot as the tie-break)
       int dev = 0;
-      for (uint32_t x = threadIdx.x; x < len; x += FNT) {
-        const uint32_t bd = bdesc[f_sub(ldsk<K>(keys_a + sizeof(K) * x))];
-        const uint32_t ng = (bd >> 11) & 127u;
-        uint32_t pos = x;
-        if (ng) {
-          const uint32_t bl = bd >> 18;
-          const uint32_t pa = cmp_a + 8 * (bd & 2047u);
-          const uint32_t me = lds16(pa + 2 * (x - bl));
-          const __half2 me2 = __ushort_as_half2_pair(me);
-          // the first two groups (sub-buckets <= 8 keys) without a loop
-          const uint2 v0 = lds64v(pa);
-          uint2 v1 = make_uint2(0x7c007c00u, 0x7c007c00u);
-          if (ng > 1) v1 = lds64v(pa + 8);
-          __half2 acc = __hadd2(__hlt2(u2h2(v0.x), me2), __hlt2(u2h2(v0.y), me2));
-          acc = __hadd2(acc, __hlt2(u2h2(v1.x), me2));
-          acc = __hadd2(acc, __hlt2(u2h2(v1.y), me2));
-          for (uint32_t g = 2; g < ng; ++g) {  // rare: larger sub-buckets
-            const uint2 v = lds64v(pa + 8 * g);
-            acc = __hadd2(acc, __hlt2(u2h2(v.x), me2));
-            acc = __hadd2(acc, __hlt2(u2h2(v.y), me2));
+#pragma unroll
+      for (int m = 0; m < FKPT; ++m) {
+        if (ds[m] != ~0u) {
+          const uint32_t cb = (ds[m] >> 13) & 511u;
+          uint32_t pos = ds[m] & 8191u;
+          if (cb) {  // cb >= 2: the number of smaller top words among the
+            // sub-bucket's composites (u32: the whole composite), four loads
+            // at once masked by the sub-bucket size
+            const uint32_t slot = ds[m] >> 22, bl = pos - slot;
+            const uint32_t a0 = keys_a + 4 * bl;  // the top words (u32: the composites)
+            const uint32_t me = (uint32_t)(key[m] >> (8 * sizeof(K) - 32));
+            const uint32_t h0 = lds32(a0), h1 = lds32(a0 + 4), h2 = lds32(a0 + 8), h3 = lds32(a0 + 12);
+            uint32_t r = (h0 < me) + (h1 < me);
+            r += (cb > 2 && h2 < me) + (cb > 3 && h3 < me);
+#pragma unroll 1
+            for (uint32_t z = 4; z < cb; ++z) r += lds32(a0 + 4 * z) < me;
+            pos = bl + r;
+            if (LOSSY) dev += (int)r - (int)slot;  // sums to 0 over a sub-bucket without ties
           }
-          const uint32_t rk = (uint32_t)__half2ushort_rz(__hadd(__low2half(acc), __high2half(acc)));
-          pos = bl + rk;
-          dev += (int)pos - (int)x;
+          sts16(pos_a + 2 * (ds[m] & 8191u), pos);
         }
-        sts16(pos_a + 2 * x, pos);
       }
       if (LOSSY) {
 #pragma unroll
         for (int o = 16; o; o >>= 1) dev += __shfl_xor_sync(0xffffffffu, dev, o);
         if (lane == 0 && dev) atomicAdd(reinterpret_cast<int*>(misc + 3), dev);
       }
-      // the ticket after the next one (its keys prefetched into L2); the next
-      // tile's keys are loaded while this tile's look-back runs, and counted
-      // and its aggregate published when this tile has been written out
-      if (d == 0) {
-        const uint32_t tw = atomicAdd(&c->fticket, 1u);
+      if (d == 0) {  // the claimed ticket: prefetch its keys into L2
         misc[1] = tw;
         if (tw < ntiles) {
           const uint4 tnw = P.ftiles[tw];
           prefetch_keys_l2(src + tnw.x, tnw.y);
         }
       }
-      __syncthreads();
+      __syncthreads();  // positions and the tie check complete
       FPROF_MARK(3);
+      if (LOSSY && misc[3] != 0) {  // (rare) tied top words
+        fused_exact(key, ds, keys_a, pos_a);
+        __syncthreads();
+      }
+      // ---- the next tile's keys load while the look-back runs
       const uint32_t tn = tq;
       tq = misc[1];
       uint32_t nprev = ~0u, nchn = 0;
@@ -2087,27 +2211,26 @@ struct Phases {
           excl = jbase[tch * 256 + d];  // first tile of its chain: published with the counts
         } else {
           excl = 0;
-#ifndef DFR_F_NOLB  // (timing experiment only: wrong output)
           if (t < regular) {
             // the regular part of the ticket order: the chain predecessors are
-            // t - chains, t - 2 chains, ...: DFR_LB of them per round trip (the
+            // t - chains, t - 2 chains, ...: DFR_FLB of them per round trip (the
             // chain's first tile is inclusive, so the walk stops there)
+            constexpr int LB = DFR_FLB;
             int tt = (int)tprev;
+            uint32_t lbv[LB];
             while (true) {
-              constexpr int LB = DFR_LB;
-              uint32_t v[LB];
 #pragma unroll
               for (int i = 0; i < LB; ++i) {
                 const int r = tt - (int)chains * i;
-                v[i] = r >= 0 ? ld_relaxed(status + (size_t)r * 256 + d) : FLAG_INC;
+                lbv[i] = r >= 0 ? ld_relaxed(status + (size_t)r * 256 + d) : FLAG_INC;
               }
               int q = 0;
               bool done = false;
 #pragma unroll
               for (; q < LB; ++q) {
-                if ((v[q] >> 30) == 0) break;
-                excl += v[q] & VAL_MASK;
-                if (v[q] & FLAG_INC) {
+                if ((lbv[q] >> 30) == 0) break;
+                excl += lbv[q] & VAL_MASK;
+                if (lbv[q] & FLAG_INC) {
                   done = true;
                   break;
                 }
@@ -2132,7 +2255,6 @@ struct Phases {
               pt = P.ftiles[pt].z;
             }
           }
-#endif
 #ifdef DFR_LB_STATS
           if (d == 0) atomicAdd(&g_lb_stats[2], 1ull);
 #endif
@@ -2144,11 +2266,15 @@ struct Phases {
       }
       __syncthreads();  // s_dst complete
       FPROF_MARK(4);
-      // ---- 5: this tile in final order (keys and positions read in slot order)
+      // ---- this tile in final order: one linear pass, the keys rebuilt from
+      // their composites
+      {
+        const K pre = *reinterpret_cast<const K*>(misc + 8 + 2 * cur);
 #pragma unroll 4
-      for (uint32_t x = threadIdx.x; x < len; x += FNT) {
-        const K k = ldsk<K>(keys_a + sizeof(K) * x);
-        out[(uint32_t)s_dst[digit_of(k, F_DG)] + lds16(pos_a + 2 * x)] = k;
+        for (uint32_t x = threadIdx.x; x < len; x += FNT) {
+          const K cpt = ld_comp(keys_a, x);
+          out[(uint32_t)s_dst[g_hi(cpt)] + lds16(pos_a + 2 * x)] = g_key(cpt, pre);
+        }
       }
       // the next tile's keys have arrived meanwhile: count them, publish its aggregate
       count_keys(lenn, cur ^ 1u);
@@ -2156,42 +2282,10 @@ struct Phases {
       publish(tn, cur ^ 1u, nprev, nchn);
       FPROF_MARK(5);
 #ifdef DFR_FPROF
-      if (threadIdx.x == 0) { fp_[8]++; fp_[9] += misc[3] != 0; }
+      if (threadIdx.x == 0) fp_[8]++;
 #endif
-      if (LOSSY && misc[3] != 0) {
-        // (rare) tied composites in this tile: a sub-bucket of c keys at bl
-        // whose positions do not sum to c*bl + c(c-1)/2 is re-ranked exactly
-        uint32_t bad = 0;
-        {
-          const uint4 b4 = reinterpret_cast<const uint4*>(bdesc)[d];
-          const uint32_t bds[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-            if (small && cs[r] >= 2) {
-              const uint32_t bl = bds[r] >> 18;
-              uint32_t ps = 0;
-              for (uint32_t y = bl; y < bl + cs[r]; ++y) ps += lds16(pos_a + 2 * y);
-              bad |= (uint32_t)(ps != cs[r] * bl + cs[r] * (cs[r] - 1) / 2) << r;
-            }
-        }
-        {
-          if (bad) atomicOr(&flag[d >> 3], bad << (4 * (d & 7)));
-          __syncthreads();
-          const uint32_t* cntc = cnt_of(cur);
-          for (uint32_t fw = w; fw < FNS / 32; fw += FNW) {
-            uint32_t bits = flag[fw];
-            while (bits) {
-              const uint32_t sb = fw * 32 + __ffs(bits) - 1;
-              bits &= bits - 1;
-              fused_fix(keys_a, bdesc[sb] >> 18, cntc[sb], out + (uint32_t)s_dst[sb >> FSB]);
-            }
-          }
-          __syncthreads();
-          if (d < FNS / 32) flag[d] = 0;
-        }
-      }
       // this tile's counters are read by no one any more
-      reinterpret_cast<uint4*>(cnt_of(cur))[d] = make_uint4(0, 0, 0, 0);
+      zero_counts(cur);
       t = tn;
       len = lenn;
       tprev = nprev;

@@ -10,7 +10,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 out = (ctypes.c_uint64 * 16)()
 dfr.lib().dfr_debug_fprof(out)
-names = ["tail(prev)", "p2 layout", "p3 stores", "p4 rank+claim", "lookback+load", "p5 write+count", "tie/fix"]
+names = ["tail(prev)", "layout", "comp stores+lb issue", "rank", "lookback+claim+load", "write+count", "zero"]
 tot = sum(out[i] for i in range(7))
 for i, n in enumerate(names):
     print(f"{n:16s} {out[i] / tot * 100:5.1f}%  cycles/tile {out[i] / max(1, out[8]):8.0f}")
