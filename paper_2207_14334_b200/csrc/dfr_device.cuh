@@ -300,6 +300,14 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
+// predicated shared load: ~0u when !pred (no access)
+__device__ __forceinline__ uint32_t lds32_if(uint32_t a, bool pred) {
+  uint32_t v = ~0u;
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.u32 %0, [%1];\n}"
+               : "+r"(v)
+               : "r"(a), "r"((uint32_t)pred));
+  return v;
+}
 __device__ __forceinline__ uint2 lds64v(uint32_t a) {
   uint2 v;
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));

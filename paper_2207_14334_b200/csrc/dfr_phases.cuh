@@ -2170,13 +2170,15 @@ struct Phases {
             const uint32_t slot = ds[m] >> 22, bl = pos - slot;
             const uint32_t a0 = keys_a + 4 * bl;  // the top words (u32: the composites)
             const uint32_t me = (uint32_t)(key[m] >> (8 * sizeof(K) - 32));
-            const uint32_t h0 = lds32(a0), h1 = lds32(a0 + 4), h2 = lds32(a0 + 8), h3 = lds32(a0 + 12);
-            uint32_t r = (h0 < me) + (h1 < me);
-            r += (cb > 2 && h2 < me) + (cb > 3 && h3 < me);
+            // (words past the sub-bucket: predicated off, read as ~0u)
+            const uint32_t h0 = lds32(a0), h1 = lds32(a0 + 4), h2 = lds32_if(a0 + 8, cb > 2),
+                           h3 = lds32_if(a0 + 12, cb > 3);
+            const uint32_t r = (h0 < me) + (h1 < me) + (h2 < me) + (h3 < me);
+            uint32_t rr = r;
 #pragma unroll 1
-            for (uint32_t z = 4; z < cb; ++z) r += lds32(a0 + 4 * z) < me;
-            pos = bl + r;
-            if (LOSSY) dev += (int)r - (int)slot;  // sums to 0 over a sub-bucket without ties
+            for (uint32_t z = 4; z < cb; ++z) rr += lds32(a0 + 4 * z) < me;
+            pos = bl + rr;
+            if (LOSSY) dev += (int)rr - (int)slot;  // sums to 0 over a sub-bucket without ties
           }
           sts16(pos_a + 2 * (ds[m] & 8191u), pos);
         }
