@@ -538,7 +538,7 @@ struct Phases {
     V val[SC_KPT];
     uint32_t dr[SC_KPT];
     const uint32_t tc_s = smem_u32(tcount);
-    uns = !PAIRS && uns;
+    uns = (!PAIRS && uns) || FRM == 2;  // FRM 2: every tile lies in one bucket of the lower digit
     if (uns) {  // (R5) rank = the tile counter's old value: keys of equal digit in any order
 #pragma unroll
       for (int jj = 0; jj < SC_KPT; ++jj) {
@@ -547,7 +547,11 @@ struct Phases {
         dr[jj] = (FULL || idx < cnt) ? digit_of(key[jj], dg) : 256u;
         if (FULL || idx < cnt) {
           dr[jj] |= atom_add_shared(tc_s + 4 * dr[jj], 1u) << 16;
-          if (FRM) red_add_shared(nh_s + 4 * digit_of(key[jj], dg + 1), 1u);
+          if (FRM == 1) red_add_shared(nh_s + 4 * digit_of(key[jj], dg + 1), 1u);
+          if (FRM == 2)  // (top digit, top 3 bits of this one), see fr_joint_addr
+            red_add_shared(fr_joint_addr(smem_u32(whist), nh_s,
+                                         digit_of(key[jj], dg + 1) * FR_CHAINS + (dr[jj] & 0xffu) / (256 / FR_CHAINS)),
+                           1u);
         }
       }
     } else {
@@ -559,7 +563,7 @@ struct Phases {
         dr[jj] = (FULL || idx < cnt) ? digit_of(key[jj], dg) : 256u;
         if (FULL || idx < cnt) {
           red_add_shared(tc_s + 4 * dr[jj], 1u);  // tile histogram
-          if (FRM) red_add_shared(nh_s + 4 * digit_of(key[jj], dg + 1), 1u);  // the next digit (Alg. 3 l.5-6)
+          if (FRM == 1) red_add_shared(nh_s + 4 * digit_of(key[jj], dg + 1), 1u);  // the next digit (Alg. 3 l.5-6)
         }
       }
     }
@@ -981,7 +985,12 @@ struct Phases {
                                                   s_dst, s_warp, dst, dstv, bstart, perm, sup,
                                                   smem_u32(nh), uns);
       if (PERM) {  // single buffer: refill it once every thread is done with the write-out
-        for (int e = threadIdx.x; e < (SC_W + 1) * 256; e += SC_NT) whist[e] = 0;
+        if (FRM == 2) {  // rows 1..SC_W-1 hold the joint counters: only row 0 and the tile counts
+          whist[threadIdx.x] = 0;
+          whist[SC_W * 256 + threadIdx.x] = 0;
+        } else {
+          for (int e = threadIdx.x; e < (SC_W + 1) * 256; e += SC_NT) whist[e] = 0;
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
           fence_proxy_async();
@@ -996,10 +1005,32 @@ struct Phases {
       mbar_inval(&bar[0]);
       mbar_inval(&bar[1]);
     }
-    if (FRM) {  // this CTA's next-digit counts (Fast Radix)
+    if (FRM == 1) {  // this CTA's next-digit counts (Fast Radix)
       __syncthreads();
       const uint32_t v = nh[threadIdx.x];
-      if (v) atomicAdd(&P.fr_cnt[(FRM == 2 ? 256 : 0) + threadIdx.x], v);
+      if (v) atomicAdd(&P.fr_cnt[threadIdx.x], v);
+    }
+    if (FRM == 2) {
+      __syncthreads();
+      fr_joint_flush(P, whist, nh);
+    }
+  }
+  // Fast Radix, pass mid (FRM 2): the (top digit, top 3 bits of the middle
+  // digit) counts of the fused pass's FR_CHAINS chains (what the histogram
+  // kernel counts on the counted path; their marginal gives the top digit's
+  // bucket offsets, Alg. 3 l.5-6): 2048 counters in the deal's unused warp
+  // rows 1..7 (1792) and the next-digit row (256), flushed once per CTA into
+  // P.J[top digit][chain] (the first FR_CHAINS of the F_CHAINS slots)
+  static constexpr int FR_CHAINS = 8;
+  static __device__ __forceinline__ uint32_t fr_joint_addr(uint32_t whist_a, uint32_t nh_a, uint32_t b) {
+    return b < 1792u ? whist_a + 4 * (256u + b) : nh_a + 4 * (b - 1792u);
+  }
+  static __device__ __forceinline__ void fr_joint_flush(const Params<K>& P, uint32_t* whist, uint32_t* nh) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t b = threadIdx.x * 8 + e;
+      const uint32_t v = b < 1792u ? whist[256 + b] : nh[b - 1792u];
+      if (v) atomicAdd(&P.J[(b / FR_CHAINS) * F_CHAINS + b % FR_CHAINS], v);
     }
   }
 
@@ -1019,6 +1050,14 @@ struct Phases {
 
   // grid: the level-0 segment's route and flags, zeroed status rows, chunk
   // table, counters and the fused pass's joint histogram
+  static __device__ __forceinline__ void zero_words(uint32_t* p, size_t n, uint32_t gid, uint32_t gsz) {
+    const size_t head = min(n, (size_t)(((16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15) / 4));
+    for (size_t x = gid; x < head; x += gsz) p[x] = 0;
+    uint4* q = reinterpret_cast<uint4*>(p + head);
+    const size_t nv = (n - head) / 4;
+    for (size_t x = gid; x < nv; x += gsz) q[x] = make_uint4(0, 0, 0, 0);
+    for (size_t x = head + 4 * nv + gid; x < n; x += gsz) p[x] = 0;
+  }
   static __device__ void fr_prep(const Params<K>& P) {
     Ctl* c = P.ctl;
     const uint32_t gid = blockIdx.x * blockDim.x + threadIdx.x, gsz = gridDim.x * blockDim.x;
@@ -1036,8 +1075,9 @@ struct Phases {
       c->fr_tiles = 0;
       c->fr_overflow = 0;
     }
-    for (size_t x = gid; x < 3 * P.status_stride; x += gsz) P.status[x] = 0;
-    for (size_t x = gid; x < (size_t)256 * P.fr_kmax; x += gsz) P.fr_ct[x] = 0;
+    // (16-byte stores: the status rows and the chunk table are ~0.26 GB at 2^28)
+    zero_words(P.status, 3 * P.status_stride, gid, gsz);
+    zero_words(P.fr_ct, (size_t)256 * P.fr_kmax, gid, gsz);
     for (uint32_t x = gid; x < 512u; x += gsz) P.fr_cnt[x] = 0;
     for (uint32_t x = gid; x < 65536u; x += gsz) P.H[x] = 0;
   }
@@ -1768,12 +1808,15 @@ struct Phases {
       s_w2[w] = b;
     }
     if (lane == 0) s_m[w] = mx;
+    // chains: 16 (top 4 bits of the middle digit) from the histogram kernel's
+    // joint counts; Fast Radix: 8 (top 3 bits) from the middle pass's
+    const uint32_t chains = P.fr ? (uint32_t)FR_CHAINS : (uint32_t)F_CHAINS;
     // chain bases per top digit: exclusive over the chains
     if (t < 256) {
       uint32_t acc = 0;
 #pragma unroll
       for (int ch = 0; ch < F_CHAINS; ++ch) {
-        const uint32_t x = P.J[t * F_CHAINS + ch];
+        const uint32_t x = (uint32_t)ch < chains ? P.J[t * F_CHAINS + ch] : 0u;
         P.J[4096 + ch * 256 + t] = acc;
         acc += x;
       }
@@ -1786,21 +1829,22 @@ struct Phases {
       ntl += s_w2[e];
       gmx = max(gmx, s_m[e]);
     }
-    // Fast Radix mode counts no chain histogram: one chain in s-run order
-    const uint32_t chains = P.fr ? 1u : (uint32_t)F_CHAINS;
-    // tiles per chain (2 warps per chain) and this thread's first index in its chain
+    // tiles per chain (32 / chains warps per chain) and this thread's first index in its chain
+    const uint32_t wpc = 32 / chains;
     uint32_t nch[F_CHAINS];
 #pragma unroll
-    for (int ch = 0; ch < F_CHAINS; ++ch) nch[ch] = s_w2[2 * ch] + s_w2[2 * ch + 1];
-    const int ch = chains == 1 ? 0 : t >> 6;
-    uint32_t jb = b - nz + ((w & 1) ? s_w2[w - 1] : 0u);  // non-empty s-runs before mine in my chain
-    uint32_t pb = 0;
-    for (int e = 0; e < w; ++e) pb += s_w2[e];
-    if (chains == 1) jb = pb + b - nz;  // the global index
+    for (int ch = 0; ch < F_CHAINS; ++ch) {
+      nch[ch] = 0;
+      if ((uint32_t)ch < chains)
+        for (uint32_t e = 0; e < wpc; ++e) nch[ch] += s_w2[ch * wpc + e];
+    }
+    const int ch = (int)(w / wpc);
+    uint32_t jb = b - nz;  // non-empty s-runs before mine in my chain
+    for (uint32_t e = ch * wpc; e < (uint32_t)w; ++e) jb += s_w2[e];
     uint32_t nmin = nch[0];
 #pragma unroll
-    for (int e = 1; e < F_CHAINS; ++e) nmin = min(nmin, nch[e]);
-    if (chains == 1) nmin = ntl;
+    for (int e = 1; e < F_CHAINS; ++e)
+      if ((uint32_t)e < chains) nmin = min(nmin, nch[e]);
     // ticket of the j-th tile of chain ch: round robin over the chains that
     // still have tiles (while every chain has: chains * j + ch)
     auto ticket = [&](uint32_t j) {
@@ -1808,11 +1852,16 @@ struct Phases {
       uint32_t p = 0;
 #pragma unroll
       for (int e = 0; e < F_CHAINS; ++e) p += min(nch[e], j) + ((e < ch && nch[e] > j) ? 1u : 0u);
-      return p;
+      return p;  // (chains beyond `chains` have nch = 0)
     };
-    if (P.fr) {  // the top digit's bucket offsets from its counts (taken in the middle pass)
+    if (P.fr) {  // the top digit's bucket offsets from the joint counts taken in the middle pass
       __shared__ uint32_t s_c[256];
-      if (t < 256) s_c[t] = P.fr_cnt[256 + t];
+      if (t < 256) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int ch = 0; ch < FR_CHAINS; ++ch) m += P.J[t * F_CHAINS + ch];
+        s_c[t] = m;
+      }
       __syncthreads();
       if (t < 256) {
         uint32_t e = 0;
