@@ -158,13 +158,19 @@ __global__ void __launch_bounds__(Phases<K, PAIRS>::DV_NT, DFR_DV_MINB) k_divert
 }
 
 template <class K, bool PAIRS>
+__global__ void __launch_bounds__(256) k_hfix(const __grid_constant__ Params<K> P) {
+  pdl_enter();
+  Phases<K, PAIRS>::hfix(P);
+}
+
+template <class K, bool PAIRS>
 __global__ void __launch_bounds__(1024) k_fplan(const __grid_constant__ Params<K> P) {
   pdl_enter();
   Phases<K, PAIRS>::fplan(P);
 }
 
 template <class K, bool PAIRS>
-__global__ void __launch_bounds__(Phases<K, PAIRS>::FNT, 3) k_fused(const __grid_constant__ Params<K> P) {
+__global__ void __launch_bounds__(Phases<K, PAIRS>::GNT, Phases<K, PAIRS>::GMINB) k_fused(const __grid_constant__ Params<K> P) {
   extern __shared__ __align__(16) uint32_t sm[];
   pdl_enter();
   Phases<K, PAIRS>::fused(P, sm);
@@ -349,7 +355,7 @@ static cudaError_t get_dev(Dev& out) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ph::SMEM_FUSED_X);
       if (err == cudaSuccess)
         err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ_fused, (const void*)k_fused<K, PAIRS>,
-                                                            Ph::FNT, Ph::SMEM_FUSED_X);
+                                                            Ph::GNT, Ph::SMEM_FUSED_X);
     }
     setup((const void*)k_levels<K, PAIRS>, Ph::SMEM_LEVEL, &d.occ_levels);
     if (err == cudaSuccess && !PAIRS) {  // keys-only mid rounds: FNT-thread CTAs
@@ -603,10 +609,11 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
         continue;
       }
       if (fuse && j == 2) {  // run-aligned tiles, then the fused last deal + diversion
+        if (!fr) launch_pdl(k_hfix<K, PAIRS>, 256, 256, 0, st, P);
         launch_pdl(k_fplan<K, PAIRS>, 1, 1024, 0, st, P);
         const int g_f = sms * std::max(1, dv.occ_fused);
-        launch_pdl(k_fused<K, PAIRS>, g_f, Ph::FNT, Ph::SMEM_FUSED_X, st, P);
-        g_launches += 2;
+        launch_pdl(k_fused<K, PAIRS>, g_f, Ph::GNT, Ph::SMEM_FUSED_X, st, P);
+        g_launches += fr ? 2 : 3;
       }
       if (fuse && j == 1 && !PAIRS)
         launch_pdl(k_scatter_fh<K>, g_sc, Ph::SC_NT, Ph::SMEM_SCATTER_P, st, P, j);

@@ -58,6 +58,9 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_LB_EARLY
 #define DFR_LB_EARLY 0  // deal: the look-back's first round trip issued before the reorder
 #endif
+#ifndef DFR_FUSED_NT
+#define DFR_FUSED_NT 512  // fused pass: threads per CTA (2 CTAs/SM at 64 registers)
+#endif
 #ifndef DFR_HIST_COPIES
 #define DFR_HIST_COPIES 1  // histogram: shared-memory counter sets per CTA (warp w uses w % copies)
 #endif

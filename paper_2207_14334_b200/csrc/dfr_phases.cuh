@@ -572,7 +572,9 @@ struct Phases {
       const K* tk = sk + (PERM ? (sup & 0xffu) : 0u);
       const uint32_t lo0 = digit_of(tk[0], s.low), lo1 = digit_of(tk[cnt - 1], s.low);
       if (lo0 == lo1) {  // input sorted by the digit below: the whole tile shares it
-        if (threadIdx.x < 256 && tcount[threadIdx.x])
+        // (counted path: fplan takes these counts from the look-back's
+        // inclusive prefixes instead; Fast Radix tiles follow a table)
+        if (FRM == 2 && threadIdx.x < 256 && tcount[threadIdx.x])
           atomicAdd(&P.H[threadIdx.x * 256 + lo0], tcount[threadIdx.x]);
       } else {  // a tile across a boundary of the digit below (one per run of it)
         for (uint32_t i = threadIdx.x; i < cnt; i += SC_NT) {
@@ -1763,6 +1765,28 @@ struct Phases {
   // earlier: its inclusive prefix is nearly always published by then, and
   // the look-back rarely waits (one chain through all 65536 tiles cannot keep
   // up with the rate at which tiles arrive).
+  // Grid of 256 CTAs (lo value l) x 256 threads (mid value d), before fplan
+  // on the counted path: the middle pass added to H[mid][lo] only the tiles
+  // that straddle a run of lo; the whole tiles [a, b) inside the run of lo = l
+  // added nothing, and their digit counts are differences of the inclusive
+  // prefixes the look-back left in the status rows: H[d][l] += I(b-1, d) - I(a-1, d)
+  static __device__ void hfix(const Params<K>& P) {
+    Ctl* c = P.ctl;
+    const Seg s = P.segq[c->cur][0];
+    if (!(P.fuse && c->level == 0 && c->nseg == 1 && s.p == 3 && (s.flags & 0xfu) == 0)) return;
+    const uint32_t l = blockIdx.x, d = threadIdx.x;
+    const uint32_t* st1 = P.status + P.status_stride;
+    const uint32_t* lofs = P.hist + (size_t)s.hist_off * 256;  // lo bucket offsets (plan2)
+    const uint32_t r0 = lofs[l], r1 = l == 255u ? s.len : lofs[l + 1];
+    // tiles [a, b) lie inside [r0, r1) (the segment's last tile may be partial)
+    const uint32_t a = (r0 + TILE - 1) / TILE, b = r1 == s.len ? (r1 + TILE - 1) / TILE : r1 / TILE;
+    if (b > a) {
+      const uint32_t ib = st1[(size_t)(b - 1) * 256 + d] & VAL_MASK;
+      const uint32_t ia = a ? st1[(size_t)(a - 1) * 256 + d] & VAL_MASK : 0u;
+      if (ib - ia) atomicAdd(&P.H[d * 256 + l], ib - ia);
+    }
+  }
+
   static __device__ void fplan(const Params<K>& P) {
     Ctl* c = P.ctl;
     __shared__ uint32_t s_w[32], s_w2[32], s_m[32];
@@ -1917,8 +1941,9 @@ struct Phases {
     }
   }
 
-  // exclusive scan of one value per thread over FNT threads with one barrier;
+  // exclusive scan of one value per thread over NW warps with one barrier;
   // s_warp must not be reused before the caller's next barrier
+  template <int NW = FNW>
   static __device__ __forceinline__ uint32_t fused_scan(uint32_t v, uint32_t* s_warp) {
     const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     uint32_t x = v;
@@ -1929,11 +1954,14 @@ struct Phases {
     }
     if (lane == 31) s_warp[w] = x;
     __syncthreads();
-    const uint4 a = *reinterpret_cast<const uint4*>(s_warp), b = *reinterpret_cast<const uint4*>(s_warp + 4);
-    const uint32_t t[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     uint32_t pre = 0;
 #pragma unroll
-    for (int e = 0; e < FNW; ++e) pre += (uint32_t)e < w ? t[e] : 0u;
+    for (int q = 0; q < NW / 4; ++q) {
+      const uint4 a = reinterpret_cast<const uint4*>(s_warp)[q];
+      const uint32_t t[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) pre += (uint32_t)(4 * q + e) < w ? t[e] : 0u;
+    }
     return pre + x - v;
   }
 
@@ -1975,7 +2003,11 @@ struct Phases {
   static constexpr int G_SBS = 8 * F_LOW - GSB;             // lowest sub-bucket bit
   static constexpr int G_CSH = 8 * (int)sizeof(K) - G_SBS;  // remaining bits -> top of c
   static_assert(G_CSH >= 13 + 8 + GSB, "composite fields: slot (13 bits) and sub-bucket");
-  static_assert(GNS / 256 == 8 || GNS / 256 == 4, "4 or 8 sub-buckets per digit value");
+  static_assert(GNS / 256 == 16 || GNS / 256 == 8 || GNS / 256 == 4, "4, 8 or 16 sub-buckets per digit value");
+  static constexpr int GNT = DFR_FUSED_NT;                // threads per fused CTA (256 or 512)
+  static constexpr int GKPT = (FT_MAX + GNT - 1) / GNT;   // keys per thread
+  static constexpr int GMINB = GNT >= 512 ? 2 : 3;        // fused CTAs per SM
+  static_assert(GNT % 128 == 0 && GNT / 32 <= 16, "fused CTA size");
   struct FX {                                              // shared-memory layout, byte offsets
     static constexpr int KEYS = 0;                         // K[FT_MAX + 4] composites (4 pad: rank loads)
     static constexpr int POS = KEYS + (FT_MAX + 4) * (int)sizeof(K);  // u16[FT_MAX]: final tile position
@@ -2034,10 +2066,10 @@ struct Phases {
   // exact ranks of every key of the tile in a small sub-bucket: full
   // composites, the slot breaking ties (the tile had tied top words)
   // (inlined: the register arrays must not be passed by address)
-  static __device__ __forceinline__ void fused_exact(const K (&key)[FKPT], const uint32_t (&ds)[FKPT],
+  static __device__ __forceinline__ void fused_exact(const K (&key)[GKPT], const uint32_t (&ds)[GKPT],
                                                      uint32_t keys_a, uint32_t pos_a) {
 #pragma unroll
-    for (int m = 0; m < FKPT; ++m) {
+    for (int m = 0; m < GKPT; ++m) {
       if (ds[m] == ~0u) continue;
       const uint32_t cb = (ds[m] >> 13) & 511u;
       if (!cb) continue;
@@ -2070,12 +2102,13 @@ struct Phases {
     uint32_t* status = P.status + (size_t)j * P.status_stride;
     const K* src = P.kbuf(route_src(sv, j)) + sv.start;
     K* const out = P.A;
-    const uint32_t d = threadIdx.x;  // layout, look-back: one thread per digit value
-    const uint32_t brow = P.hist[(size_t)(sv.hist_off + j) * 256 + d];  // bucket offsets of the top digit
-    const uint32_t kofs = w * 32 * FKPT + lane;  // this thread's first key of a tile
+    const uint32_t d = threadIdx.x;  // layout, look-back: one thread per digit value (d < 256)
+    const bool dig = d < 256;
+    const uint32_t brow = dig ? P.hist[(size_t)(sv.hist_off + j) * 256 + d] : 0u;  // bucket offsets of the top digit
+    const uint32_t kofs = w * 32 * GKPT + lane;  // this thread's first key of a tile
     auto cnt_of = [&](uint32_t cb) { return reinterpret_cast<uint32_t*>(base + FX::CNT + cb * GNS * 4); };
-    K key[FKPT];
-    uint32_t ds[FKPT];  // sub-bucket | slot << SBW; then slot position | compare count << 13 | slot << 22;
+    K key[GKPT];
+    uint32_t ds[GKPT];  // sub-bucket | slot << SBW; then slot position | compare count << 13 | slot << 22;
                         // then final position; ~0u: no key
     // keys of tile tt -> registers, with the tile's chain link and chain
     auto load_keys = [&](uint32_t tt, uint32_t& prev, uint32_t& chn) -> uint32_t {
@@ -2088,7 +2121,7 @@ struct Phases {
         const K* p = src + td.x + kofs;
         const int lim = (int)ln - (int)kofs;
 #pragma unroll
-        for (int m = 0; m < FKPT; ++m) key[m] = m * 32 < lim ? p[m * 32] : K(0);
+        for (int m = 0; m < GKPT; ++m) key[m] = m * 32 < lim ? p[m * 32] : K(0);
       }
       return ln;
     };
@@ -2097,7 +2130,7 @@ struct Phases {
       const int lim = (int)ln - (int)kofs;
       const uint32_t ca = cnt0_a + cb * GNS * 4;
 #pragma unroll
-      for (int m = 0; m < FKPT; ++m) {
+      for (int m = 0; m < GKPT; ++m) {
         ds[m] = ~0u;
         if (m * 32 < lim) {
           const uint32_t sb = g_sub(key[m]);
@@ -2110,7 +2143,7 @@ struct Phases {
       const uint4* p = reinterpret_cast<const uint4*>(cnt_of(cb)) + (GNS / 1024) * d;
 #pragma unroll
       for (int r = 0; r < GNS / 1024; ++r) {
-        const uint4 v = p[r];
+        const uint4 v = dig ? p[r] : make_uint4(0, 0, 0, 0);
         cs[4 * r] = v.x;
         cs[4 * r + 1] = v.y;
         cs[4 * r + 2] = v.z;
@@ -2123,7 +2156,7 @@ struct Phases {
     const uint32_t* jbase = P.J + 4096;
     const uint32_t regular = c->fused_regular, chains = c->fused_chains;
     auto publish = [&](uint32_t tt, uint32_t cb, uint32_t prev, uint32_t chn) {
-      if (tt < ntiles) {
+      if (tt < ntiles && dig) {
         uint32_t cs[GNS / 256];
         digit_counts(cb, cs);
         uint32_t cdd = 0;
@@ -2134,6 +2167,7 @@ struct Phases {
       }
     };
     auto zero_counts = [&](uint32_t cb) {
+      if (!dig) return;
       uint4* p = reinterpret_cast<uint4*>(cnt_of(cb)) + (GNS / 1024) * d;
 #pragma unroll
       for (int r = 0; r < GNS / 1024; ++r) p[r] = make_uint4(0, 0, 0, 0);
@@ -2170,7 +2204,7 @@ struct Phases {
       for (int r = 0; r < GNS / 256; ++r) cd += cs[r];
       const bool small = cd <= nd;
       if (d == 0) misc[3] = 0;  // the tile's tie check (the last tile's was read before this barrier)
-      const uint32_t lst = fused_scan(cd, s_warp);  // the bucket's first tile position
+      const uint32_t lst = fused_scan<GNT / 32>(cd, s_warp);  // the bucket's first tile position
       {
         uint32_t so = lst, bd[GNS / 256];
 #pragma unroll
@@ -2180,7 +2214,8 @@ struct Phases {
         }
         uint4* bp = reinterpret_cast<uint4*>(bdesc) + (GNS / 1024) * d;
 #pragma unroll
-        for (int r = 0; r < GNS / 1024; ++r) bp[r] = make_uint4(bd[4 * r], bd[4 * r + 1], bd[4 * r + 2], bd[4 * r + 3]);
+        for (int r = 0; r < GNS / 1024; ++r)
+          if (dig) bp[r] = make_uint4(bd[4 * r], bd[4 * r + 1], bd[4 * r + 2], bd[4 * r + 3]);
       }
       __syncthreads();
       FPROF_MARK(1);
@@ -2190,7 +2225,7 @@ struct Phases {
       if (d == 0) tw = atomicAdd(&c->fticket, 1u);
       // ---- composites at their slot positions
 #pragma unroll
-      for (int m = 0; m < FKPT; ++m) {
+      for (int m = 0; m < GKPT; ++m) {
         if (ds[m] != ~0u) {
           const uint32_t sb = ds[m] & (GNS - 1), slot = ds[m] >> SBW;
           const uint32_t bd = bdesc[sb];
@@ -2209,7 +2244,7 @@ struct Phases {
       // re-ranked exactly on the full composites (slot as the tie-break)
       int dev = 0;
 #pragma unroll
-      for (int m = 0; m < FKPT; ++m) {
+      for (int m = 0; m < GKPT; ++m) {
         if (ds[m] != ~0u) {
           const uint32_t cb = (ds[m] >> 13) & 511u;
           uint32_t pos = ds[m] & 8191u;
@@ -2256,7 +2291,7 @@ struct Phases {
       uint32_t nprev = ~0u, nchn = 0;
       const uint32_t lenn = load_keys(tn, nprev, nchn);
       // ---- decoupled look-back along this tile's chain (thread d, digit d)
-      {
+      if (dig) {
         uint32_t excl;
         if (tprev == ~0u) {
           excl = jbase[tch * 256 + d];  // first tile of its chain: published with the counts
@@ -2322,7 +2357,7 @@ struct Phases {
       {
         const K pre = *reinterpret_cast<const K*>(misc + 8 + 2 * cur);
 #pragma unroll 4
-        for (uint32_t x = threadIdx.x; x < len; x += FNT) {
+        for (uint32_t x = threadIdx.x; x < len; x += GNT) {
           const K cpt = ld_comp(keys_a, x);
           out[(uint32_t)s_dst[g_hi(cpt)] + lds16(pos_a + 2 * x)] = g_key(cpt, pre);
         }
