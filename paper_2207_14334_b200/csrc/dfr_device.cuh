@@ -61,6 +61,9 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_FUSED_NT
 #define DFR_FUSED_NT 512  // fused pass: threads per CTA (2 CTAs/SM at 64 registers)
 #endif
+#ifndef DFR_RUN_ATOMS
+#define DFR_RUN_ATOMS 0  // atomic deal ranks: one atomic per run of equal digits in consecutive lanes
+#endif
 #ifndef DFR_HIST_COPIES
 #define DFR_HIST_COPIES 1  // histogram: shared-memory counter sets per CTA (warp w uses w % copies)
 #endif

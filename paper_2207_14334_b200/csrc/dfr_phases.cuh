@@ -545,6 +545,28 @@ struct Phases {
         const uint32_t idx = w * 32 * SC_KPT + jj * 32 + lane;
         key[jj] = sk[(PERM ? (sup & 0xffu) : 0u) + idx];
         dr[jj] = (FULL || idx < cnt) ? digit_of(key[jj], dg) : 256u;
+#if DFR_RUN_ATOMS
+        // runs of equal digits in consecutive lanes (locally sorted input)
+        // reserve their ranks with one atomic per run instead of serializing
+        // on the counter
+        const uint32_t dprev = __shfl_up_sync(0xffffffffu, dr[jj], 1);
+        const uint32_t bsame = __ballot_sync(0xffffffffu, lane > 0 && dr[jj] == dprev);
+        if (bsame) {
+          const uint32_t starts = ~bsame, le = 0xffffffffu >> (31 - lane);
+          const uint32_t st0 = 31 - __clz(starts & le), nxt = starts & ~le;
+          const uint32_t rlen = (nxt ? (uint32_t)__ffs(nxt) - 1u : 32u) - st0;
+          uint32_t old = 0;
+          if (lane == st0 && (FULL || idx < cnt)) old = atom_add_shared(tc_s + 4 * dr[jj], rlen);
+          old = __shfl_sync(0xffffffffu, old, st0);
+          if (FULL || idx < cnt) dr[jj] |= (old + lane - st0) << 16;
+          if (FRM == 1 && (FULL || idx < cnt)) red_add_shared(nh_s + 4 * digit_of(key[jj], dg + 1), 1u);
+          if (FRM == 2 && (FULL || idx < cnt))
+            red_add_shared(fr_joint_addr(smem_u32(whist), nh_s,
+                                         digit_of(key[jj], dg + 1) * FR_CHAINS + (dr[jj] & 0xffu) / (256 / FR_CHAINS)),
+                           1u);
+          continue;
+        }
+#endif
         if (FULL || idx < cnt) {
           dr[jj] |= atom_add_shared(tc_s + 4 * dr[jj], 1u) << 16;
           if (FRM == 1) red_add_shared(nh_s + 4 * digit_of(key[jj], dg + 1), 1u);
@@ -902,6 +924,7 @@ struct Phases {
     // the segment record and its bucket-offset row are re-read only when a
     // tile of another segment comes up (level 0: once per CTA)
     uint32_t cur_si = ~0u, bstart = 0;
+    bool skewed = false;  // the segment's digit of this pass is skewed: stable ranks
     Seg s;
 
     if (PERM) {
@@ -921,8 +944,16 @@ struct Phases {
       if (si != cur_si) {
         cur_si = si;
         s = q[si];
-        if (threadIdx.x < 256 && pass_active(s, j) && FRM != 1)
+        uint32_t cntd = 0;
+        if (threadIdx.x < 256 && pass_active(s, j) && FRM != 1) {
           bstart = P.hist[(size_t)(s.hist_off + j) * 256 + threadIdx.x];
+          const uint32_t nx = threadIdx.x == 255 ? s.len : P.hist[(size_t)(s.hist_off + j) * 256 + threadIdx.x + 1];
+          cntd = nx - bstart;
+        }
+        // a skewed digit (> 1/16 of the segment) puts many lanes of a warp on
+        // one tile counter: the atomic ranks (R5) would serialize on it, the
+        // ballot multi-split does not
+        skewed = __syncthreads_or(cntd > s.len / 16) != 0;
       }
       const bool tma = ti[cb * 4 + 2] != 0;
       const uint32_t sup = (PERM && tma) ? ti[3] : 0u;  // the tile's offsets in the aligned copy
@@ -969,7 +1000,7 @@ struct Phases {
       // (R5) keys only: ranks in any order when the tile is constant in the
       // group digits below dg (the input of pass j is sorted by them)
       bool uns = false;
-      if (!PAIRS && P.unstable) {
+      if (!PAIRS && P.unstable && !skewed) {
         if (j == 0) {
           uns = true;
         } else {

@@ -1,2 +1,2 @@
-DFR_LIB=build/var/libdfr_nt512sb4.so timeout 900 python -m pytest -q -x tests/test_gpu_fused.py > gpurun_out/nt_pytest.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/nt_pytest.log
-bash tools/gpu_variants.sh nt512sb4 2>&1 | grep -E "^(base|nt)"
+timeout 1200 python tools/sweeps.py nd --out gpurun_out/r02b_sweep_nd.jsonl > gpurun_out/sw_nd.log 2>&1; echo "nd rc=$?"
+timeout 1200 python tools/sweeps.py paper --out gpurun_out/r02b_sweep_paper.jsonl > gpurun_out/sw_paper.log 2>&1; echo "paper rc=$?"

@@ -26,6 +26,19 @@ __global__ void scatter_k(const uint64_t* __restrict__ a, uint64_t* __restrict__
   }
 }
 
+// the same streams, but lane-scattered: consecutive keys of a tile go to
+// different streams (key i -> stream i % 256, position i / 256 in its run), so
+// every warp store touches 32 runs (a deal writing straight from registers)
+__global__ void scatter_lanes_k(const uint64_t* __restrict__ a, uint64_t* __restrict__ b, size_t n) {
+  const size_t tiles = n / 4096, stream_len = n / 256;
+  for (size_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (int i = threadIdx.x; i < 4096; i += 256) {
+      const size_t o = (size_t)(i % 256) * stream_len + t * 16 + i / 256;
+      b[o] = a[t * 4096 + i];
+    }
+  }
+}
+
 int main() {
   const size_t n = (size_t)1 << 28;
   uint64_t *a, *b;
@@ -53,6 +66,7 @@ int main() {
   timeit("scatter S=256 R=16", [&] { scatter_k<16><<<sms * 8, 256>>>(a, b, n, 256); });
   timeit("scatter S=256 R=32", [&] { scatter_k<32><<<sms * 8, 256>>>(a, b, n, 128); });
   timeit("scatter S=64 R=64", [&] { scatter_k<64><<<sms * 8, 256>>>(a, b, n, 64); });
+  timeit("lane-scattered S=256 R=16", [&] { scatter_lanes_k<<<sms * 8, 256>>>(a, b, n); });
   cudaError_t e = cudaGetLastError();
   printf("%s\n", cudaGetErrorString(e));
   return 0;

@@ -6,7 +6,8 @@
         (256^3.75 = 2^30 is beyond this build's n < 2^30)
   python tools/sweeps.py nd [--out F]      N_d in {16..256} on c5-uniform / c3
         inputs, and the ablations: separate last pass (no fusion), every pass
-        run (no pass skipping), full LSD over all digits (u32)
+        run (no pass skipping), every deal stable (stable_deals), Fast Radix
+        estimation, full LSD over all digits (u32)
 
 Each cell: 2 warm-up sorts, then 5 timed sorts, each of a pristine resident
 copy (CUDA events around the library call, allocation inside); median ms and
@@ -99,6 +100,11 @@ def main():
                   **measure(dfr, torch, k, fused=False, reps=args.reps)})
             emit({"sweep": "ablation", "case": case, "n": n, "variant": "no pass skipping",
                   **measure(dfr, torch, k, skip_trivial=False, reps=args.reps)})
+            emit({"sweep": "ablation", "case": case, "n": n, "variant": "stable deals (stable_deals=1)",
+                  **measure(dfr, torch, k, stable_deals=True, reps=args.reps)})
+            if n >= 1 << 27:
+                emit({"sweep": "ablation", "case": case, "n": n, "variant": "Fast Radix estimation",
+                      **measure(dfr, torch, k, fast_radix=True, reps=args.reps)})
             del k
             torch.cuda.empty_cache()
         k = datagen.uniform_u32(1 << 27, 31)
@@ -106,6 +112,8 @@ def main():
               **measure(dfr, torch, k, reps=args.reps)})
         emit({"sweep": "ablation", "case": "u32 uniform", "n": 1 << 27, "variant": "full LSD (4 passes)",
               **measure(dfr, torch, k, full_lsd=True, reps=args.reps)})
+        emit({"sweep": "ablation", "case": "u32 uniform", "n": 1 << 27, "variant": "Fast Radix estimation",
+              **measure(dfr, torch, k, fast_radix=True, reps=args.reps)})
     if args.out:
         with open(args.out, "w") as f:
             for r in rows:
