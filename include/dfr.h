@@ -46,11 +46,12 @@ enum {
                              overlapping keys/values, or a bad dfr_config field */
   DFR_ERR_ALLOC = -2,     /* scratch allocation failed (SPEC's "resource error") */
   DFR_ERR_CUDA = -3,      /* a CUDA launch/configuration error (cudaGetLastError) */
-  DFR_ERR_TOO_LARGE = -4  /* n >= 2^30 (the packed 30-bit look-back counts) */
+  DFR_ERR_TOO_LARGE = -4  /* n > 2^30 = 256^3.75, the paper's largest N: look-back
+                             counts are packed in 30 bits and summed mod 2^30 */
 };
 
 /* Limits of this build. */
-#define DFR_MAX_N ((size_t)1 << 30) /* exclusive */
+#define DFR_MAX_N ((size_t)1 << 30) /* inclusive */
 #define DFR_RADIX_BITS 8            /* M = 256 */
 #define DFR_DEFAULT_ND 64           /* diversion threshold N_d */
 

@@ -521,7 +521,7 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
     const char* va = reinterpret_cast<const char*>(vals);
     if (ka < va + n * 4 && va < ka + n * sizeof(K)) return DFR_ERR_INVALID;
   }
-  if (n >= DFR_MAX_N) return DFR_ERR_TOO_LARGE;
+  if (n > DFR_MAX_N) return DFR_ERR_TOO_LARGE;
   Dev dv;
   if (get_dev<K, PAIRS>(dv) != cudaSuccess) return DFR_ERR_CUDA;
   cudaGetLastError();
@@ -532,7 +532,8 @@ static int sort_impl(K* keys, uint32_t* vals, size_t n, cudaStream_t st, const d
   // digits (s-runs of about n / 2^16 >= 2048 keys fill a tile)
   const bool fuse = !PAIRS && !nofuse && p0 == 3 && n >= ((size_t)1 << 27);
   // Fast Radix estimation (Alg. 3): on the fused level-0 path
-  const bool fr = fuse && fast_radix && !full_lsd;
+  // (a bucket total of exactly 2^30 would read back as 0 from the 30-bit status)
+  const bool fr = fuse && fast_radix && !full_lsd && n < DFR_MAX_N;
   const Layout L = make_layout(n, sizeof(K), PAIRS ? 4 : 0, n_d, full_lsd ? (int)sizeof(K) : 1, fuse, fr);
   char* ws = nullptr;
   if (cudaMallocAsync(reinterpret_cast<void**>(&ws), L.total, st) != cudaSuccess) {
@@ -681,7 +682,7 @@ static int stage_impl(const K* in, const uint32_t* vin, K* out, uint32_t* vout, 
                       int digit_lo, int p, uint32_t* d_counts, cudaStream_t st) {
   using Ph = Phases<K, PAIRS>;
   if (n == 0) return DFR_OK;
-  if (n >= DFR_MAX_N) return DFR_ERR_TOO_LARGE;
+  if (n > DFR_MAX_N) return DFR_ERR_TOO_LARGE;
   if (!in || p < 1 || p > MAX_PASSES || digit_lo < 0 || digit_lo + p > (int)sizeof(K))
     return DFR_ERR_INVALID;
   Dev dv;
@@ -741,7 +742,7 @@ static int sort_pairs_u64(unsigned long long* keys, unsigned long long* vals, si
     const char* va = reinterpret_cast<const char*>(vals);
     if (ka < va + n * 8 && va < ka + n * 8) return DFR_ERR_INVALID;
   }
-  if (n >= DFR_MAX_N) return DFR_ERR_TOO_LARGE;
+  if (n > DFR_MAX_N) return DFR_ERR_TOO_LARGE;
   Dev dv;
   if (get_dev<unsigned long long, true>(dv) != cudaSuccess) return DFR_ERR_CUDA;
   char* ws = nullptr;

@@ -717,8 +717,10 @@ struct Phases {
           if (k == 0) __nanosleep(DFR_LB_SLEEP);  // predecessor not published: yield the issue slots
           tt -= k;
         }
-        st_relaxed(status + (size_t)t * 256 + dd, FLAG_INC | (excl + run));
+        st_relaxed(status + (size_t)t * 256 + dd, FLAG_INC | ((excl + run) & VAL_MASK));
       }
+      // counts are mod 2^30 (n <= 2^30): a non-empty run's prefix is < 2^30
+      excl &= VAL_MASK;
       // run offset of the digit relative to the tile's local offsets, mod 2^32
       // (Fast Radix estimated pass: the rank inside the digit's bucket)
       s_dst[dd] = FRM == 1 ? (int)(excl - lstart) : (int)(s.start + bstart + excl - lstart);
@@ -1814,7 +1816,8 @@ struct Phases {
     if (b > a) {
       const uint32_t ib = st1[(size_t)(b - 1) * 256 + d] & VAL_MASK;
       const uint32_t ia = a ? st1[(size_t)(a - 1) * 256 + d] & VAL_MASK : 0u;
-      if (ib - ia) atomicAdd(&P.H[d * 256 + l], ib - ia);
+      const uint32_t dif = (ib - ia) & VAL_MASK;  // mod 2^30 (n <= 2^30)
+      if (dif) atomicAdd(&P.H[d * 256 + l], dif);
     }
   }
 
@@ -2194,7 +2197,7 @@ struct Phases {
 #pragma unroll
         for (int r = 0; r < GNS / 256; ++r) cdd += cs[r];
         st_relaxed(status + (size_t)tt * 256 + d,
-                   prev == ~0u ? (FLAG_INC | (jbase[chn * 256 + d] + cdd)) : (FLAG_AGG | cdd));
+                   prev == ~0u ? (FLAG_INC | ((jbase[chn * 256 + d] + cdd) & VAL_MASK)) : (FLAG_AGG | cdd));
       }
     };
     auto zero_counts = [&](uint32_t cb) {
@@ -2375,8 +2378,9 @@ struct Phases {
 #ifdef DFR_LB_STATS
           if (d == 0) atomicAdd(&g_lb_stats[2], 1ull);
 #endif
-          st_relaxed(status + (size_t)t * 256 + d, FLAG_INC | (excl + cd));
+          st_relaxed(status + (size_t)t * 256 + d, FLAG_INC | ((excl + cd) & VAL_MASK));
         }
+        excl &= VAL_MASK;  // mod 2^30 (n <= 2^30): exact for a non-empty bucket
         const uint32_t gstart = sv.start + brow + excl;  // global index of bucket (d, this s-run)
         s_dst[d] = (int)(gstart - lst);
         if (!small) push_bucket(P, sv, 0u, gstart, cd);  // written to A below (Alg. 4 l.11)

@@ -61,6 +61,12 @@ def test_trivial_calls_need_no_device():
     assert L.dfr_sort_u64(None, 10, None) == dfr.DFR_ERR_INVALID
     # misaligned element pointer
     assert L.dfr_sort_u64(ctypes.c_void_p(0x1004), 10, None) == dfr.DFR_ERR_INVALID
+    # size bound: n <= 2^30 = 256^3.75 (the paper's largest N) is accepted
+    # by the checks; one more key is DFR_ERR_TOO_LARGE before any device work
+    assert L.dfr_sort_u64(ctypes.c_void_p(0x1000), (1 << 30) + 1, None) == dfr.DFR_ERR_TOO_LARGE
+    assert L.dfr_sort_u32(ctypes.c_void_p(0x1000), (1 << 30) + 1, None) == dfr.DFR_ERR_TOO_LARGE
+    assert L.dfr_sort_pairs_u64(ctypes.c_void_p(0x1000), ctypes.c_void_p(0x10000000000),
+                                (1 << 30) + 1, None) == dfr.DFR_ERR_TOO_LARGE
 
 
 def test_product_has_no_oracle_dependency():
