@@ -79,6 +79,9 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_DV_CU
 #define DFR_DV_CU 1  // diversion rank-count loop unroll
 #endif
+#ifndef DFR_FRANK8
+#define DFR_FRANK8 1  // fused pass: sub-bucket words 4..7 compared in one round trip
+#endif
 #ifndef DFR_FLB
 #define DFR_FLB 4  // fused pass: look-back predecessors loaded per round trip
 #endif

@@ -2293,8 +2293,18 @@ struct Phases {
                            h3 = lds32_if(a0 + 12, cb > 3);
             const uint32_t r = (h0 < me) + (h1 < me) + (h2 < me) + (h3 < me);
             uint32_t rr = r;
+#if DFR_FRANK8
+            if (cb > 4) {  // words 4..7 in one round trip; a longer sub-bucket loops (rare)
+              const uint32_t h4 = lds32(a0 + 16), h5 = lds32_if(a0 + 20, cb > 5),
+                             h6 = lds32_if(a0 + 24, cb > 6), h7 = lds32_if(a0 + 28, cb > 7);
+              rr += (h4 < me) + (h5 < me) + (h6 < me) + (h7 < me);
+#pragma unroll 1
+              for (uint32_t z = 8; z < cb; ++z) rr += lds32(a0 + 4 * z) < me;
+            }
+#else
 #pragma unroll 1
             for (uint32_t z = 4; z < cb; ++z) rr += lds32(a0 + 4 * z) < me;
+#endif
             pos = bl + rr;
             if (LOSSY) dev += (int)rr - (int)slot;  // sums to 0 over a sub-bucket without ties
           }
