@@ -59,7 +59,7 @@ constexpr int WARPS = THREADS / 32;
 #define DFR_LB_EARLY 0  // deal: the look-back's first round trip issued before the reorder
 #endif
 #ifndef DFR_FUSED_NT
-#define DFR_FUSED_NT 512  // fused pass: threads per CTA (2 CTAs/SM at 64 registers)
+#define DFR_FUSED_NT 256  // fused pass: threads per CTA (3 CTAs/SM)
 #endif
 #ifndef DFR_RUN_ATOMS
 #define DFR_RUN_ATOMS 0  // atomic deal ranks: one atomic per run of equal digits in consecutive lanes
