@@ -19,3 +19,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_fused|k_scatter|k_hist" -s 0 -c 4 \
   -o gpurun_out/${TAG}_full python bench.py --quick --steps 1 --warmup 1 --no-cold > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "done rc=$?"
+timeout 900 python tools/sweeps.py paper --out gpurun_out/${TAG}_sweep_paper.jsonl > gpurun_out/${TAG}_sweep_paper.log 2>&1; echo "sweep rc=$?"

@@ -2,8 +2,8 @@
 """Measured sweeps on one B200.
 
   python tools/sweeps.py paper [--out F]   the paper's workloads (P:288, P:313,
-        P:337; 16-byte records S:22-27) at N = 256^3, 256^3.25, 256^3.5, 2^29
-        (256^3.75 = 2^30 is beyond this build's n < 2^30)
+        P:337; 16-byte records S:22-27) at N = 256^3, 256^3.25, 256^3.5, 2^29,
+        256^3.75 = 2^30 (records up to 2^28)
   python tools/sweeps.py nd [--out F]      N_d in {16..256} on c5-uniform / c3
         inputs, and the ablations: separate last pass (no fusion), every pass
         run (no pass skipping), every deal stable (stable_deals), Fast Radix
@@ -83,7 +83,7 @@ def main():
 
     if args.what == "paper":
         for case in ["paper-uniform", "paper-wide-normal", "paper-narrow-normal", "paper-records"]:
-            for n in [1 << 24, 1 << 26, 1 << 28, 1 << 29]:
+            for n in [1 << 24, 1 << 26, 1 << 28, 1 << 29, 1 << 30]:
                 if case == "paper-records" and n > 1 << 28:
                     continue
                 k, v = datagen.make_case(case, n)
