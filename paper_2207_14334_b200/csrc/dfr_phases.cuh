@@ -1256,7 +1256,8 @@ struct Phases {
   static constexpr int DV_CMP = 4 * WIN + 64;  // halves
 
   struct DivertSmem {
-    char* win[2];       // double-buffered windows: keys, then values (pairs)
+    char* win[2];       // window buffers (keys, then values for pairs); both point at one
+                        // buffer: 8 CTAs/SM hide its refill (divert())
     uint16_t* cmp;      // fp16 composites
     uint16_t* order;    // slot -> window position of the key ranked there
     uint32_t* bm;       // bucket-start bitmask (4 zero words on each side)
