@@ -82,6 +82,12 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_FRANK8
 #define DFR_FRANK8 1  // fused pass: sub-bucket words 4..7 compared in one round trip
 #endif
+#ifndef DFR_FRANK_SB
+#define DFR_FRANK_SB 1  // fused pass: ranks by one thread per sub-bucket (<= 4 keys branch-free; longer ones via a work list)
+#endif
+#ifndef DFR_FLOAD_EARLY
+#define DFR_FLOAD_EARLY 1  // fused pass (with DFR_FRANK_SB): the next tile's keys load during the ranks
+#endif
 #ifndef DFR_FLB
 #define DFR_FLB 4  // fused pass: look-back predecessors loaded per round trip
 #endif
@@ -334,6 +340,12 @@ __device__ __forceinline__ unsigned long long ldsk<unsigned long long>(uint32_t 
 }
 __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+// predicated 16-bit shared store (no access when !pred)
+__device__ __forceinline__ void sts16_if(uint32_t a, uint32_t v, bool pred) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.shared.u16 [%0], %1;\n}" ::"r"(a),
+               "h"((unsigned short)v), "r"((uint32_t)pred)
+               : "memory");
 }
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");

@@ -2051,9 +2051,15 @@ struct Phases {
     static constexpr int SDST = BDESC + GNS * 4;           // int[256]
     static constexpr int WARP = SDST + 1024;               // u32[16]
     static constexpr int MISC = WARP + 64;                 // u32[16]: tickets; [8..11] the two tiles' prefixes
+#if DFR_FRANK_SB
+    static constexpr int WL = MISC + 64;                   // u32[G_WL]: sub-buckets of > 4 keys (start | count << 13)
+    static constexpr int BYTES = WL + (FT_MAX / 5 + 5) * 4;
+#else
     static constexpr int BYTES = MISC + 64;
+#endif
   };
   static_assert(FX::CNT % 16 == 0 && FX::BDESC % 16 == 0 && FX::MISC % 16 == 0, "fused smem alignment");
+  static_assert(FX::BYTES + 1024 <= 233472 / 3, "three exact-composite fused CTAs per SM");
   static constexpr size_t SMEM_FUSED_X = FX::BYTES;
   static constexpr K G_PRE = (K(1) << (8 * F_DG)) - (K(1) << (8 * F_LOW));  // the (mid, lo) bits
   static __device__ __forceinline__ uint32_t g_sub(K k) {
@@ -2101,20 +2107,37 @@ struct Phases {
   // exact ranks of every key of the tile in a small sub-bucket: full
   // composites, the slot breaking ties (the tile had tied top words)
   // (inlined: the register arrays must not be passed by address)
-  static __device__ __forceinline__ void fused_exact(const K (&key)[GKPT], const uint32_t (&ds)[GKPT],
-                                                     uint32_t keys_a, uint32_t pos_a) {
+  static __device__ __forceinline__ void fused_exact(const uint32_t (&ds)[GKPT], uint32_t keys_a, uint32_t pos_a) {
 #pragma unroll
     for (int m = 0; m < GKPT; ++m) {
       if (ds[m] == ~0u) continue;
       const uint32_t cb = (ds[m] >> 13) & 511u;
       if (!cb) continue;
       const uint32_t x = ds[m] & 8191u, slot = ds[m] >> 22, bl = x - slot;
+      const K me = ld_comp(keys_a, x);  // this key's composite, still at its slot position
       uint32_t r = 0;
       for (uint32_t z = 0; z < cb; ++z) {
         const K cz = ld_comp(keys_a, bl + z);
-        r += cz < key[m] || (cz == key[m] && z < slot);
+        r += cz < me || (cz == me && z < slot);
       }
       sts16(pos_a + 2 * x, bl + r);
+    }
+  }
+
+  // the same from the sub-bucket descriptors (start | count << 13; count 0: a
+  // large bucket, kept in slot order), 8 threads per sub-bucket
+  static __device__ DFR_COLD void fused_exact_sb(const uint32_t* bdesc, uint32_t keys_a, uint32_t pos_a) {
+    for (uint32_t e = threadIdx.x; e < (uint32_t)GNS * 8; e += GNT) {
+      const uint32_t bd = bdesc[e >> 3], cb = bd >> 13, bl = bd & 8191u;
+      for (uint32_t s = e & 7u; s < cb; s += 8) {
+        const K me = ld_comp(keys_a, bl + s);
+        uint32_t r = 0;
+        for (uint32_t z = 0; z < cb; ++z) {
+          const K cz = ld_comp(keys_a, bl + z);
+          r += cz < me || (cz == me && z < s);
+        }
+        sts16(pos_a + 2 * (bl + s), bl + r);
+      }
     }
   }
 
@@ -2137,6 +2160,9 @@ struct Phases {
     uint32_t* status = P.status + (size_t)j * P.status_stride;
     const K* src = P.kbuf(route_src(sv, j)) + sv.start;
     K* const out = P.A;
+#if DFR_FRANK_SB
+    const uint32_t wl_a = smem_u32(base + FX::WL);
+#endif
     const uint32_t d = threadIdx.x;  // layout, look-back: one thread per digit value (d < 256)
     const bool dig = d < 256;
     const uint32_t brow = dig ? P.hist[(size_t)(sv.hist_off + j) * 256 + d] : 0u;  // bucket offsets of the top digit
@@ -2239,6 +2265,27 @@ struct Phases {
       for (int r = 0; r < GNS / 256; ++r) cd += cs[r];
       const bool small = cd <= nd;
       if (d == 0) misc[3] = 0;  // the tile's tie check (the last tile's was read before this barrier)
+#if DFR_FRANK_SB
+      // sub-buckets of > 4 keys are ranked from a work list: their count rides
+      // in the scan's upper half (both totals < 2^16)
+      uint32_t nl = 0;
+#pragma unroll
+      for (int r = 0; r < GNS / 256; ++r) nl += small && cs[r] > 4;
+      const uint32_t ex = fused_scan<GNT / 32>(cd | nl << 16, s_warp);
+      const uint32_t lst = ex & 0xffffu;  // the bucket's first tile position
+      if (d == 255) misc[4] = (ex >> 16) + nl;
+      {
+        uint32_t so = lst, wo = wl_a + 4 * (ex >> 16), bd[GNS / 256];
+#pragma unroll
+        for (int r = 0; r < GNS / 256; ++r) {
+          bd[r] = so | (small ? cs[r] : 0u) << 13;  // a large bucket stays in slot order
+          if (small && cs[r] > 4) {
+            sts32(wo, bd[r]);
+            wo += 4;
+          }
+          so += cs[r];
+        }
+#else
       const uint32_t lst = fused_scan<GNT / 32>(cd, s_warp);  // the bucket's first tile position
       {
         uint32_t so = lst, bd[GNS / 256];
@@ -2247,6 +2294,7 @@ struct Phases {
           bd[r] = so | ((small && cs[r] >= 2) ? cs[r] : 0u) << 13;
           so += cs[r];
         }
+#endif
         uint4* bp = reinterpret_cast<uint4*>(bdesc) + (GNS / 1024) * d;
 #pragma unroll
         for (int r = 0; r < GNS / 1024; ++r)
@@ -2267,11 +2315,93 @@ struct Phases {
           const uint32_t x = (bd & 8191u) + slot, cb = bd >> 13;
           key[m] = g_comp(key[m], sb, slot);
           st_comp(keys_a, x, key[m]);
+#if DFR_FRANK_SB
+          if (!cb) sts16(pos_a + 2 * x, x);  // in a large bucket: slot order
+#else
           ds[m] = x | cb << 13 | (cb ? slot << 22 : 0u);
+#endif
         }
       }
       __syncthreads();
       FPROF_MARK(2);
+#if DFR_FRANK_SB
+      // ---- ranks, one thread per sub-bucket: the composites' top words (u32:
+      // the composites) of a sub-bucket of 2..4 keys are ranked against one
+      // another branch-free (words past its end predicated off, read as ~0u:
+      // never below a key's); equal words keep slot order and raise the tie
+      // flag (u64: equal keys, or keys that differ only below the top word:
+      // the tile is then re-ranked on the full composites); sub-buckets of
+      // > 4 keys come from the work list, 8 threads each
+#if DFR_FLOAD_EARLY
+      // the composites are in shared memory: the registers take the next tile's keys
+      const uint32_t tn = tq;
+      uint32_t nprev = ~0u, nchn = 0;
+      const uint32_t lenn = load_keys(tn, nprev, nchn);
+#endif
+      {
+        bool tie = false;
+        constexpr int NB = GNS / GNT >= 4 ? 4 : GNS / GNT;  // sub-buckets per batch of loads
+#pragma unroll
+        for (int i0 = 0; i0 < GNS / GNT; i0 += NB) {
+          uint32_t bd[NB], h[NB][4];
+#pragma unroll
+          for (int q = 0; q < NB; ++q) bd[q] = bdesc[(i0 + q) * GNT + threadIdx.x];
+#pragma unroll
+          for (int q = 0; q < NB; ++q) {
+            const uint32_t cb = bd[q] >> 13, a0 = keys_a + 4 * (bd[q] & 8191u);
+            const bool c2 = cb - 2u <= 2u;
+            h[q][0] = lds32_if(a0, c2);
+            h[q][1] = lds32_if(a0 + 4, c2);
+            h[q][2] = lds32_if(a0 + 8, cb - 3u <= 1u);
+            h[q][3] = lds32_if(a0 + 12, cb == 4u);
+          }
+#pragma unroll
+          for (int q = 0; q < NB; ++q) {
+            const uint32_t cb = bd[q] >> 13, bl = bd[q] & 8191u, p0 = pos_a + 2 * bl;
+            const bool c1 = cb - 1u <= 3u, c2 = cb - 2u <= 2u, c3 = cb - 3u <= 1u, c4 = cb == 4u;
+            const uint32_t h0 = h[q][0], h1 = h[q][1], h2 = h[q][2], h3 = h[q][3];
+            const uint32_t l10 = h1 < h0, l20 = h2 < h0, l30 = h3 < h0, l21 = h2 < h1, l31 = h3 < h1, l32 = h3 < h2;
+            sts16_if(p0, bl + l10 + l20 + l30, c1);
+            sts16_if(p0 + 2, bl + 1 - l10 + l21 + l31, c2);
+            sts16_if(p0 + 4, bl + 2 - l20 - l21 + l32, c3);
+            sts16_if(p0 + 6, bl + 3 - l30 - l31 - l32, c4);
+            if (LOSSY)
+              tie |= (c2 && h0 == h1) || (c3 && (h0 == h2 || h1 == h2)) || (c4 && (h0 == h3 || h1 == h3 || h2 == h3));
+          }
+        }
+        const uint32_t nwl = misc[4];
+#pragma unroll 1
+        for (uint32_t e = threadIdx.x; e < nwl * 8; e += GNT) {
+          const uint32_t bd = lds32(wl_a + 4 * (e >> 3));
+          const uint32_t cb = bd >> 13, bl = bd & 8191u, a0 = keys_a + 4 * bl;
+#pragma unroll 1
+          for (uint32_t s = e & 7u; s < cb; s += 8) {
+            const uint32_t me = lds32(a0 + 4 * s);
+            uint32_t r = 0;
+#pragma unroll 1
+            for (uint32_t z = 0; z < cb; z += 8) {  // 8 words per round trip, the ones past the end read as ~0u
+              uint32_t hz[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) hz[q] = lds32_if(a0 + 4 * (z + q), z + q < cb);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                r += hz[q] < me || (hz[q] == me && z + q < s);
+                if (LOSSY) tie |= hz[q] == me && z + q != s;
+              }
+            }
+            sts16(pos_a + 2 * (bl + s), bl + r);
+          }
+        }
+        if (LOSSY && tie) misc[3] = 1u;
+      }
+      if (d == 0) {  // the claimed ticket: prefetch its keys into L2
+        misc[1] = tw;
+        if (tw < ntiles) {
+          const uint4 tnw = P.ftiles[tw];
+          prefetch_keys_l2(src + tnw.x, tnw.y);
+        }
+      }
+#else
       // ---- ranks: the number of smaller composites in the sub-bucket.  u64:
       // the top words of equal keys (or, with odds 2^-32 per pair, of keys
       // that differ only in their low bits) tie and share the lower rank; the
@@ -2324,17 +2454,26 @@ struct Phases {
           prefetch_keys_l2(src + tnw.x, tnw.y);
         }
       }
+#endif
       __syncthreads();  // positions and the tie check complete
       FPROF_MARK(3);
       if (LOSSY && misc[3] != 0) {  // (rare) tied top words
-        fused_exact(key, ds, keys_a, pos_a);
+#if DFR_FRANK_SB
+        fused_exact_sb(bdesc, keys_a, pos_a);
+#else
+        fused_exact(ds, keys_a, pos_a);
+#endif
         __syncthreads();
       }
       // ---- the next tile's keys load while the look-back runs
+#if DFR_FRANK_SB && DFR_FLOAD_EARLY
+      tq = misc[1];
+#else
       const uint32_t tn = tq;
       tq = misc[1];
       uint32_t nprev = ~0u, nchn = 0;
       const uint32_t lenn = load_keys(tn, nprev, nchn);
+#endif
       // ---- decoupled look-back along this tile's chain (thread d, digit d)
       if (dig) {
         uint32_t excl;
