@@ -323,6 +323,26 @@ __device__ __forceinline__ uint32_t lds32_if(uint32_t a, bool pred) {
                : "r"(a), "r"((uint32_t)pred));
   return v;
 }
+// predicated on x <= lim / x < lim (the compare inside the asm: no bool materialized)
+__device__ __forceinline__ uint32_t lds32_if_le(uint32_t a, uint32_t x, uint32_t lim) {
+  uint32_t v = ~0u;
+  asm volatile("{\n .reg .pred p;\n setp.le.u32 p, %2, %3;\n @p ld.shared.u32 %0, [%1];\n}"
+               : "+r"(v)
+               : "r"(a), "r"(x), "r"(lim));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32_if_lt(uint32_t a, uint32_t x, uint32_t lim) {
+  uint32_t v = ~0u;
+  asm volatile("{\n .reg .pred p;\n setp.lt.u32 p, %2, %3;\n @p ld.shared.u32 %0, [%1];\n}"
+               : "+r"(v)
+               : "r"(a), "r"(x), "r"(lim));
+  return v;
+}
+__device__ __forceinline__ void sts16_if_le(uint32_t a, uint32_t v, uint32_t x, uint32_t lim) {
+  asm volatile("{\n .reg .pred p;\n setp.le.u32 p, %2, %3;\n @p st.shared.u16 [%0], %1;\n}" ::"r"(a),
+               "h"((unsigned short)v), "r"(x), "r"(lim)
+               : "memory");
+}
 __device__ __forceinline__ uint2 lds64v(uint32_t a) {
   uint2 v;
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));

@@ -2285,6 +2285,8 @@ struct Phases {
           }
           so += cs[r];
         }
+        if (!small)  // (rare) written in slot order
+          for (uint32_t x = lst; x < lst + cd; ++x) sts16(pos_a + 2 * x, x);
 #else
       const uint32_t lst = fused_scan<GNT / 32>(cd, s_warp);  // the bucket's first tile position
       {
@@ -2315,9 +2317,7 @@ struct Phases {
           const uint32_t x = (bd & 8191u) + slot, cb = bd >> 13;
           key[m] = g_comp(key[m], sb, slot);
           st_comp(keys_a, x, key[m]);
-#if DFR_FRANK_SB
-          if (!cb) sts16(pos_a + 2 * x, x);  // in a large bucket: slot order
-#else
+#if !DFR_FRANK_SB
           ds[m] = x | cb << 13 | (cb ? slot << 22 : 0u);
 #endif
         }
@@ -2349,27 +2349,28 @@ struct Phases {
 #pragma unroll
           for (int q = 0; q < NB; ++q) {
             const uint32_t cb = bd[q] >> 13, a0 = keys_a + 4 * (bd[q] & 8191u);
-            const bool c2 = cb - 2u <= 2u;
-            h[q][0] = lds32_if(a0, c2);
-            h[q][1] = lds32_if(a0 + 4, c2);
-            h[q][2] = lds32_if(a0 + 8, cb - 3u <= 1u);
-            h[q][3] = lds32_if(a0 + 12, cb == 4u);
+            h[q][0] = lds32_if_le(a0, cb - 2u, 2u);
+            h[q][1] = lds32_if_le(a0 + 4, cb - 2u, 2u);
+            h[q][2] = lds32_if_le(a0 + 8, cb - 3u, 1u);
+            h[q][3] = lds32_if_le(a0 + 12, cb - 4u, 0u);
           }
 #pragma unroll
           for (int q = 0; q < NB; ++q) {
             const uint32_t cb = bd[q] >> 13, bl = bd[q] & 8191u, p0 = pos_a + 2 * bl;
-            const bool c1 = cb - 1u <= 3u, c2 = cb - 2u <= 2u, c3 = cb - 3u <= 1u, c4 = cb == 4u;
             const uint32_t h0 = h[q][0], h1 = h[q][1], h2 = h[q][2], h3 = h[q][3];
             const uint32_t l10 = h1 < h0, l20 = h2 < h0, l30 = h3 < h0, l21 = h2 < h1, l31 = h3 < h1, l32 = h3 < h2;
-            sts16_if(p0, bl + l10 + l20 + l30, c1);
-            sts16_if(p0 + 2, bl + 1 - l10 + l21 + l31, c2);
-            sts16_if(p0 + 4, bl + 2 - l20 - l21 + l32, c3);
-            sts16_if(p0 + 6, bl + 3 - l30 - l31 - l32, c4);
-            if (LOSSY)
-              tie |= (c2 && h0 == h1) || (c3 && (h0 == h2 || h1 == h2)) || (c4 && (h0 == h3 || h1 == h3 || h2 == h3));
+            sts16_if_le(p0, bl + l10 + l20 + l30, cb - 1u, 3u);
+            sts16_if_le(p0 + 2, bl + 1 - l10 + l21 + l31, cb - 2u, 2u);
+            sts16_if_le(p0 + 4, bl + 2 - l20 - l21 + l32, cb - 3u, 1u);
+            sts16_if_le(p0 + 6, bl + 3 - l30 - l31 - l32, cb - 4u, 0u);
+            if (LOSSY) {  // equal words among the sub-bucket's own (the pads are equal to one another)
+              const bool e4 = h0 == h3 || h1 == h3 || h2 == h3, e3 = h0 == h2 || h1 == h2 || (cb == 4u && e4);
+              tie |= cb - 2u <= 2u && (h0 == h1 || (cb >= 3u && e3));
+            }
           }
         }
         const uint32_t nwl = misc[4];
+        int dev = 0;  // sum of (rank - slot): 0 over a sub-bucket without equal words
 #pragma unroll 1
         for (uint32_t e = threadIdx.x; e < nwl * 8; e += GNT) {
           const uint32_t bd = lds32(wl_a + 4 * (e >> 3));
@@ -2382,15 +2383,19 @@ struct Phases {
             for (uint32_t z = 0; z < cb; z += 8) {  // 8 words per round trip, the ones past the end read as ~0u
               uint32_t hz[8];
 #pragma unroll
-              for (int q = 0; q < 8; ++q) hz[q] = lds32_if(a0 + 4 * (z + q), z + q < cb);
+              for (int q = 0; q < 8; ++q) hz[q] = lds32_if_lt(a0 + 4 * (z + q), z + q, cb);
 #pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                r += hz[q] < me || (hz[q] == me && z + q < s);
-                if (LOSSY) tie |= hz[q] == me && z + q != s;
-              }
+              for (int q = 0; q < 8; ++q) r += hz[q] < me;
             }
             sts16(pos_a + 2 * (bl + s), bl + r);
+            dev += (int)r - (int)s;
           }
+        }
+        if (LOSSY) {  // the 8 threads of a sub-bucket are 8 adjacent lanes
+          dev += __shfl_xor_sync(0xffffffffu, dev, 1);
+          dev += __shfl_xor_sync(0xffffffffu, dev, 2);
+          dev += __shfl_xor_sync(0xffffffffu, dev, 4);
+          tie |= dev != 0;
         }
         if (LOSSY && tie) misc[3] = 1u;
       }
