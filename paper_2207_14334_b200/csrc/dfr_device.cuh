@@ -85,6 +85,12 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_FRANK_SB
 #define DFR_FRANK_SB 1  // fused pass: ranks by one thread per sub-bucket (<= 4 keys branch-free; longer ones via a work list)
 #endif
+#ifndef DFR_FRANK_NB
+#define DFR_FRANK_NB 4  // fused ranks: sub-buckets per batch of loads
+#endif
+#ifndef DFR_FRANK_BL
+#define DFR_FRANK_BL 2  // fused ranks: threads per long sub-bucket (each ranks 8 / BL keys of a group of 8)
+#endif
 #ifndef DFR_FLOAD_EARLY
 #define DFR_FLOAD_EARLY 1  // fused pass (with DFR_FRANK_SB): the next tile's keys load during the ranks
 #endif

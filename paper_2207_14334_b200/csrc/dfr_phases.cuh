@@ -2340,7 +2340,7 @@ struct Phases {
 #endif
       {
         bool tie = false;
-        constexpr int NB = GNS / GNT >= 4 ? 4 : GNS / GNT;  // sub-buckets per batch of loads
+        constexpr int NB = GNS / GNT >= DFR_FRANK_NB ? DFR_FRANK_NB : GNS / GNT;  // sub-buckets per batch of loads
 #pragma unroll
         for (int i0 = 0; i0 < GNS / GNT; i0 += NB) {
           uint32_t bd[NB], h[NB][4];
@@ -2371,30 +2371,44 @@ struct Phases {
         }
         const uint32_t nwl = misc[4];
         int dev = 0;  // sum of (rank - slot): 0 over a sub-bucket without equal words
+        // BL threads per long sub-bucket, each ranking keys s, s + BL, ... of a
+        // group of 8 against the same 8 loaded words
+        constexpr uint32_t BL = DFR_FRANK_BL, KPL = 8 / BL;
+        static_assert(BL == 1 || BL == 2 || BL == 4 || BL == 8, "threads per long sub-bucket");
 #pragma unroll 1
-        for (uint32_t e = threadIdx.x; e < nwl * 8; e += GNT) {
-          const uint32_t bd = lds32(wl_a + 4 * (e >> 3));
+        for (uint32_t e = threadIdx.x; e < nwl * BL; e += GNT) {
+          const uint32_t bd = lds32(wl_a + 4 * (e / BL));
           const uint32_t cb = bd >> 13, bl = bd & 8191u, a0 = keys_a + 4 * bl;
 #pragma unroll 1
-          for (uint32_t s = e & 7u; s < cb; s += 8) {
-            const uint32_t me = lds32(a0 + 4 * s);
-            uint32_t r = 0;
+          for (uint32_t s = e % BL; s < cb; s += 8) {
+            uint32_t me[KPL], r[KPL];
+#pragma unroll
+            for (uint32_t k = 0; k < KPL; ++k) {
+              me[k] = lds32_if_lt(a0 + 4 * (s + k * BL), s + k * BL, cb);
+              r[k] = 0;
+            }
 #pragma unroll 1
             for (uint32_t z = 0; z < cb; z += 8) {  // 8 words per round trip, the ones past the end read as ~0u
               uint32_t hz[8];
 #pragma unroll
               for (int q = 0; q < 8; ++q) hz[q] = lds32_if_lt(a0 + 4 * (z + q), z + q, cb);
 #pragma unroll
-              for (int q = 0; q < 8; ++q) r += hz[q] < me;
+              for (int q = 0; q < 8; ++q)
+#pragma unroll
+                for (uint32_t k = 0; k < KPL; ++k) r[k] += hz[q] < me[k];
             }
-            sts16(pos_a + 2 * (bl + s), bl + r);
-            dev += (int)r - (int)s;
+#pragma unroll
+            for (uint32_t k = 0; k < KPL; ++k)
+              if (s + k * BL < cb) {
+                sts16(pos_a + 2 * (bl + s + k * BL), bl + r[k]);
+                dev += (int)r[k] - (int)(s + k * BL);
+              }
           }
         }
-        if (LOSSY) {  // the 8 threads of a sub-bucket are 8 adjacent lanes
-          dev += __shfl_xor_sync(0xffffffffu, dev, 1);
-          dev += __shfl_xor_sync(0xffffffffu, dev, 2);
-          dev += __shfl_xor_sync(0xffffffffu, dev, 4);
+        if (LOSSY) {  // the threads of a sub-bucket are adjacent lanes
+          if (BL >= 2) dev += __shfl_xor_sync(0xffffffffu, dev, 1);
+          if (BL >= 4) dev += __shfl_xor_sync(0xffffffffu, dev, 2);
+          if (BL >= 8) dev += __shfl_xor_sync(0xffffffffu, dev, 4);
           tie |= dev != 0;
         }
         if (LOSSY && tie) misc[3] = 1u;

@@ -9,7 +9,9 @@ element by element, on inputs built to reach each of its branches:
   and global queue) next to small ones;
 * an s-run longer than a tile (the device-side fallback to the separate deal
   and diversion through the third buffer);
-* other N_d values (8-bit bucket index; small N_d)."""
+* other N_d values (8-bit bucket index; small N_d);
+* every bucket's keys in ONE sub-bucket (the work list of sub-buckets of > 4
+  keys: several 8-word groups per sub-bucket, distinct and tied top words)."""
 import numpy as np
 import pytest
 
@@ -102,3 +104,29 @@ def test_fused_other_nd(n_d):
 def test_fused_u32_nd100():
     """u32 keys with an 8-bit bucket index: lossy composites of R = 8 bits."""
     _check(datagen.uniform_u32(N, 310), 1, n_d=100)
+
+
+@pytest.mark.parametrize("n_d", [64, 256])
+def test_fused_long_sub_buckets(n_d):
+    """The 3 bits below the group digits are cleared, so the ~16 keys of every
+    bucket share one sub-bucket: all ranks come from the work list of
+    sub-buckets of > 4 keys (two or more 8-word groups each)."""
+    k = datagen.uniform_u64(N, 311) & ~np.uint64(7 << 37)
+    _check(k, 1, n_d=n_d)
+
+
+def test_fused_long_sub_buckets_ties():
+    """As above with only 2 distinct values of the composite's top word per
+    bucket and random low bits: the rank-sum check of the work list raises the
+    tie flag and the tile is re-ranked on the full composites."""
+    r = datagen.uniform_u64(N, 312)
+    k = (r & np.uint64(0xFFFFFF0000000000)) | ((r >> np.uint64(3)) & np.uint64(1)) << np.uint64(30) | (r & np.uint64(31))
+    _check(k, 1)
+
+
+def test_fused_mixed_sub_bucket_sizes_u32():
+    """u32 keys (exact, unique composites) with a skewed sub-bucket split:
+    half of the keys of a bucket in one sub-bucket."""
+    r = datagen.uniform_u32(N, 313)
+    k = np.where(r & np.uint32(1), r & ~np.uint32(7 << 5), r)
+    _check(k.astype(np.uint32), 1)
