@@ -91,6 +91,12 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_FRANK_BL
 #define DFR_FRANK_BL 2  // fused ranks: threads per long sub-bucket (each ranks 8 / BL keys of a group of 8)
 #endif
+#ifndef DFR_FWO_UNROLL
+#define DFR_FWO_UNROLL 4  // fused pass: write-out unroll
+#endif
+#ifndef DFR_FLB_EARLY
+#define DFR_FLB_EARLY 0  // fused pass: the look-back's first round trip issued before the ranks
+#endif
 #ifndef DFR_FLOAD_EARLY
 #define DFR_FLOAD_EARLY 1  // fused pass (with DFR_FRANK_SB): the next tile's keys load during the ranks
 #endif
@@ -99,7 +105,7 @@ constexpr int WARPS = THREADS / 32;
 #endif
 constexpr int LB_PAD = 32;  // status rows in front of pass 0's table (>= DFR_LB, DFR_FLB)
 static_assert(DFR_LB <= LB_PAD && DFR_FLB <= LB_PAD, "look-back pad");
-constexpr int WO_UNROLL = DFR_WO_UNROLL, DV_CU = DFR_DV_CU;
+constexpr int WO_UNROLL = DFR_WO_UNROLL, DV_CU = DFR_DV_CU, FWO_UNROLL = DFR_FWO_UNROLL;
 constexpr int HCOPIES = DFR_HIST_COPIES;
 static_assert(WARPS % HCOPIES == 0, "histogram copies");
 constexpr int KPT = 16;                  // keys per thread per tile

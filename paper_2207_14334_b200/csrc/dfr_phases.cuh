@@ -2332,6 +2332,18 @@ struct Phases {
       // flag (u64: equal keys, or keys that differ only below the top word:
       // the tile is then re-ranked on the full composites); sub-buckets of
       // > 4 keys come from the work list, 8 threads each
+#if DFR_FLB_EARLY
+      // the look-back's first round trip, in flight during the ranks (an
+      // aggregate read early is still this predecessor's aggregate)
+      uint32_t lbe[DFR_FLB];
+      if (dig && tprev != ~0u && t < regular) {
+#pragma unroll
+        for (int i = 0; i < DFR_FLB; ++i) {
+          const int r = (int)tprev - (int)chains * i;
+          lbe[i] = r >= 0 ? ld_relaxed(status + (size_t)r * 256 + d) : FLAG_INC;
+        }
+      }
+#endif
 #if DFR_FLOAD_EARLY
       // the composites are in shared memory: the registers take the next tile's keys
       const uint32_t tn = tq;
@@ -2507,7 +2519,17 @@ struct Phases {
             constexpr int LB = DFR_FLB;
             int tt = (int)tprev;
             uint32_t lbv[LB];
+#if DFR_FLB_EARLY
+            bool first = true;
+#endif
             while (true) {
+#if DFR_FLB_EARLY
+              if (first) {
+#pragma unroll
+                for (int i = 0; i < LB; ++i) lbv[i] = lbe[i];
+                first = false;
+              } else
+#endif
 #pragma unroll
               for (int i = 0; i < LB; ++i) {
                 const int r = tt - (int)chains * i;
@@ -2560,7 +2582,7 @@ struct Phases {
       // their composites
       {
         const K pre = *reinterpret_cast<const K*>(misc + 8 + 2 * cur);
-#pragma unroll 4
+#pragma unroll FWO_UNROLL
         for (uint32_t x = threadIdx.x; x < len; x += GNT) {
           const K cpt = ld_comp(keys_a, x);
           out[(uint32_t)s_dst[g_hi(cpt)] + lds16(pos_a + 2 * x)] = g_key(cpt, pre);
