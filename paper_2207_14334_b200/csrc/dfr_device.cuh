@@ -92,7 +92,7 @@ constexpr int WARPS = THREADS / 32;
 #define DFR_FRANK_BL 2  // fused ranks: threads per long sub-bucket (each ranks 8 / BL keys of a group of 8)
 #endif
 #ifndef DFR_FWO_UNROLL
-#define DFR_FWO_UNROLL 4  // fused pass: write-out unroll
+#define DFR_FWO_UNROLL 2  // fused pass: write-out unroll
 #endif
 #ifndef DFR_FLB_EARLY
 #define DFR_FLB_EARLY 0  // fused pass: the look-back's first round trip issued before the ranks
