@@ -88,6 +88,9 @@ constexpr int WARPS = THREADS / 32;
 #ifndef DFR_FRANK_NB
 #define DFR_FRANK_NB 4  // fused ranks: sub-buckets per batch of loads
 #endif
+#ifndef DFR_FRANK_MA
+#define DFR_FRANK_MA 4  // fused ranks: sub-buckets of up to this many keys are ranked branch-free by their own thread
+#endif
 #ifndef DFR_FRANK_BL
 #define DFR_FRANK_BL 2  // fused ranks: threads per long sub-bucket (each ranks 8 / BL keys of a group of 8)
 #endif

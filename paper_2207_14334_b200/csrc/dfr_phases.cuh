@@ -2060,6 +2060,7 @@ struct Phases {
   };
   static_assert(FX::CNT % 16 == 0 && FX::BDESC % 16 == 0 && FX::MISC % 16 == 0, "fused smem alignment");
   static_assert(FX::BYTES + 1024 <= 233472 / 3, "three exact-composite fused CTAs per SM");
+  static_assert(DFR_FRANK_MA >= 4 && DFR_FRANK_MA <= 8, "work list capacity FT_MAX / 5; ranks branch-free up to 8 keys");
   static constexpr size_t SMEM_FUSED_X = FX::BYTES;
   static constexpr K G_PRE = (K(1) << (8 * F_DG)) - (K(1) << (8 * F_LOW));  // the (mid, lo) bits
   static __device__ __forceinline__ uint32_t g_sub(K k) {
@@ -2270,7 +2271,7 @@ struct Phases {
       // in the scan's upper half (both totals < 2^16)
       uint32_t nl = 0;
 #pragma unroll
-      for (int r = 0; r < GNS / 256; ++r) nl += small && cs[r] > 4;
+      for (int r = 0; r < GNS / 256; ++r) nl += small && cs[r] > (uint32_t)DFR_FRANK_MA;
       const uint32_t ex = fused_scan<GNT / 32>(cd | nl << 16, s_warp);
       const uint32_t lst = ex & 0xffffu;  // the bucket's first tile position
       if (d == 255) misc[4] = (ex >> 16) + nl;
@@ -2279,7 +2280,7 @@ struct Phases {
 #pragma unroll
         for (int r = 0; r < GNS / 256; ++r) {
           bd[r] = so | (small ? cs[r] : 0u) << 13;  // a large bucket stays in slot order
-          if (small && cs[r] > 4) {
+          if (small && cs[r] > (uint32_t)DFR_FRANK_MA) {
             sts32(wo, bd[r]);
             wo += 4;
           }
@@ -2355,29 +2356,43 @@ struct Phases {
         constexpr int NB = GNS / GNT >= DFR_FRANK_NB ? DFR_FRANK_NB : GNS / GNT;  // sub-buckets per batch of loads
 #pragma unroll
         for (int i0 = 0; i0 < GNS / GNT; i0 += NB) {
-          uint32_t bd[NB], h[NB][4];
+          constexpr int MA = DFR_FRANK_MA;  // longest sub-bucket ranked here
+          uint32_t bd[NB], h[NB][MA];
 #pragma unroll
           for (int q = 0; q < NB; ++q) bd[q] = bdesc[(i0 + q) * GNT + threadIdx.x];
 #pragma unroll
           for (int q = 0; q < NB; ++q) {
             const uint32_t cb = bd[q] >> 13, a0 = keys_a + 4 * (bd[q] & 8191u);
-            h[q][0] = lds32_if_le(a0, cb - 2u, 2u);
-            h[q][1] = lds32_if_le(a0 + 4, cb - 2u, 2u);
-            h[q][2] = lds32_if_le(a0 + 8, cb - 3u, 1u);
-            h[q][3] = lds32_if_le(a0 + 12, cb - 4u, 0u);
+#pragma unroll
+            for (int i = 0; i < MA; ++i) {  // word i: 2 <= cb <= MA and i < cb
+              const uint32_t lo = i < 1 ? 2u : (uint32_t)i + 1u;
+              h[q][i] = lds32_if_le(a0 + 4 * i, cb - lo, (uint32_t)MA - lo);
+            }
           }
 #pragma unroll
           for (int q = 0; q < NB; ++q) {
             const uint32_t cb = bd[q] >> 13, bl = bd[q] & 8191u, p0 = pos_a + 2 * bl;
-            const uint32_t h0 = h[q][0], h1 = h[q][1], h2 = h[q][2], h3 = h[q][3];
-            const uint32_t l10 = h1 < h0, l20 = h2 < h0, l30 = h3 < h0, l21 = h2 < h1, l31 = h3 < h1, l32 = h3 < h2;
-            sts16_if_le(p0, bl + l10 + l20 + l30, cb - 1u, 3u);
-            sts16_if_le(p0 + 2, bl + 1 - l10 + l21 + l31, cb - 2u, 2u);
-            sts16_if_le(p0 + 4, bl + 2 - l20 - l21 + l32, cb - 3u, 1u);
-            sts16_if_le(p0 + 6, bl + 3 - l30 - l31 - l32, cb - 4u, 0u);
+            uint32_t r[MA];
+#pragma unroll
+            for (int i = 0; i < MA; ++i) r[i] = bl + i;
+#pragma unroll
+            for (int i = 0; i < MA; ++i)
+#pragma unroll
+              for (int k = i + 1; k < MA; ++k) {  // equal words keep slot order
+                const uint32_t l = h[q][k] < h[q][i];
+                r[i] += l;
+                r[k] -= l;
+              }
+#pragma unroll
+            for (int i = 0; i < MA; ++i) sts16_if_le(p0 + 2 * i, r[i], cb - (i + 1), (uint32_t)(MA - (i + 1)));
             if (LOSSY) {  // equal words among the sub-bucket's own (the pads are equal to one another)
-              const bool e4 = h0 == h3 || h1 == h3 || h2 == h3, e3 = h0 == h2 || h1 == h2 || (cb == 4u && e4);
-              tie |= cb - 2u <= 2u && (h0 == h1 || (cb >= 3u && e3));
+#pragma unroll
+              for (int k = 1; k < MA; ++k) {
+                bool e = false;
+#pragma unroll
+                for (int i = 0; i < k; ++i) e |= h[q][i] == h[q][k];
+                tie |= e && cb - (k + 1) <= (uint32_t)(MA - (k + 1));
+              }
             }
           }
         }
