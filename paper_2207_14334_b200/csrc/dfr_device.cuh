@@ -83,7 +83,7 @@ constexpr int WARPS = THREADS / 32;
 #define DFR_FRANK8 1  // fused pass: sub-bucket words 4..7 compared in one round trip
 #endif
 #ifndef DFR_FRANK_SB
-#define DFR_FRANK_SB 1  // fused pass: ranks by one thread per sub-bucket (<= 4 keys branch-free; longer ones via a work list)
+#define DFR_FRANK_SB 1  // fused pass: ranks by one thread per sub-bucket (<= DFR_FRANK_MA keys branch-free; longer ones via a work list; 0: one thread per key, r02c)
 #endif
 #ifndef DFR_FRANK_NB
 #define DFR_FRANK_NB 4  // fused ranks: sub-buckets per batch of loads

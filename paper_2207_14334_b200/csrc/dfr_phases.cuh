@@ -2052,7 +2052,7 @@ struct Phases {
     static constexpr int WARP = SDST + 1024;               // u32[16]
     static constexpr int MISC = WARP + 64;                 // u32[16]: tickets; [8..11] the two tiles' prefixes
 #if DFR_FRANK_SB
-    static constexpr int WL = MISC + 64;                   // u32[G_WL]: sub-buckets of > 4 keys (start | count << 13)
+    static constexpr int WL = MISC + 64;                   // u32[FT_MAX / 5 + 5]: sub-buckets of > DFR_FRANK_MA keys (start | count << 13)
     static constexpr int BYTES = WL + (FT_MAX / 5 + 5) * 4;
 #else
     static constexpr int BYTES = MISC + 64;
@@ -2267,7 +2267,7 @@ struct Phases {
       const bool small = cd <= nd;
       if (d == 0) misc[3] = 0;  // the tile's tie check (the last tile's was read before this barrier)
 #if DFR_FRANK_SB
-      // sub-buckets of > 4 keys are ranked from a work list: their count rides
+      // sub-buckets of > DFR_FRANK_MA (4) keys are ranked from a work list: their count rides
       // in the scan's upper half (both totals < 2^16)
       uint32_t nl = 0;
 #pragma unroll
@@ -2327,12 +2327,16 @@ struct Phases {
       FPROF_MARK(2);
 #if DFR_FRANK_SB
       // ---- ranks, one thread per sub-bucket: the composites' top words (u32:
-      // the composites) of a sub-bucket of 2..4 keys are ranked against one
+      // the composites) of a sub-bucket of 2..MA (4) keys are ranked against one
       // another branch-free (words past its end predicated off, read as ~0u:
-      // never below a key's); equal words keep slot order and raise the tie
-      // flag (u64: equal keys, or keys that differ only below the top word:
-      // the tile is then re-ranked on the full composites); sub-buckets of
-      // > 4 keys come from the work list, 8 threads each
+      // never below a key's): every pair is compared once, the loser of a
+      // compare moving up and the other down from the slot order, so equal
+      // words keep slot order; equal words raise the tie flag (u64: equal
+      // keys, or keys that differ only below the top word: the tile is then
+      // re-ranked on the full composites).  Longer sub-buckets come from the
+      // work list, DFR_FRANK_BL (2) threads each, every thread ranking 4 keys
+      // of a group of 8 against the same 8 loaded words; a tie there makes the
+      // sum of (rank - slot) over the sub-bucket non-zero
 #if DFR_FLB_EARLY
       // the look-back's first round trip, in flight during the ranks (an
       // aggregate read early is still this predecessor's aggregate)
